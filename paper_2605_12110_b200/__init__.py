@@ -1,0 +1,13 @@
+"""B200-native AB-Sparse decode-time block-sparse attention (sm_100a CUDA behind a C ABI).
+
+See DESIGN.md. The numeric path lives in lib/libabsp.so (built from csrc/ by
+build.py); this package is the Python host mirror of the reference API.
+"""
+from .absparse import (BlockAssignment, CentroidMethod, DecodeAttention, EngineConfig,  # noqa: F401
+                       QuantMode, QuantSpec, build_offsets, fill_synthetic_bf16)
+from ._abi import (AbspError, CapacityError, CudaError, InvalidArgument, LogicError,  # noqa: F401
+                   OutOfRange)
+
+__all__ = ["BlockAssignment", "CentroidMethod", "DecodeAttention", "EngineConfig", "QuantMode",
+           "QuantSpec", "build_offsets", "fill_synthetic_bf16", "AbspError", "CapacityError",
+           "CudaError", "InvalidArgument", "LogicError", "OutOfRange"]

@@ -1,0 +1,611 @@
+// C-ABI host layer (include/absp.h): validation with the reference's error
+// semantics, per-layer device state, and stream-ordered kernel orchestration.
+//
+// Nothing here computes on the host: every numeric result comes from the
+// sm_100a kernels in this directory. There is no CPU fallback; a missing or
+// failing device surfaces as ABSP_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "absp_internal.cuh"
+
+using namespace absp;
+
+namespace {
+
+thread_local std::string g_err;
+
+absp_status fail(absp_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+absp_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(ABSP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define ABSP_CUDA(call)                                             \
+    do {                                                            \
+        cudaError_t e__ = (call);                                   \
+        if (e__ != cudaSuccess) return cuda_fail(e__, #call);       \
+    } while (0)
+
+uint32_t ceil_div(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t count) {
+        if (count <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        if (count == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct Layer {
+    bool assigned = false, bound = false, built = false;
+    std::vector<uint32_t> block_sizes;
+    const uint16_t* k_pool = nullptr;
+    const uint16_t* v_pool = nullptr;
+    uint64_t pool_pages = 0;
+    const uint32_t* page_table = nullptr;
+    uint32_t max_pages = 0;
+    uint32_t batch = 0;
+    std::vector<uint32_t> seq_lens;
+    std::vector<UnitDesc> desc;
+    std::vector<ScoreItem> items;
+    uint64_t total_cap = 0, total_centroids = 0;
+    uint32_t max_cap = 0, max_nblocks = 0, max_budget = 0, max_select = 0, step_chunks = 0;
+    uint32_t sel_stride = 0;
+
+    DevBuf<UnitDesc> d_desc;
+    DevBuf<ScoreItem> d_items;
+    DevBuf<float> values, values_min, scales, zps, scales_min, zps_min, scores;
+    DevBuf<uint32_t> codes, codes_min;
+    DevBuf<uint32_t> sel_blocks, sel_counts;
+    DevBuf<float> part_o, part_ml;
+    DevBuf<uint16_t> stage_q;
+    DevBuf<float> stage_out;
+
+    void release() {
+        d_desc.release(); d_items.release();
+        values.release(); values_min.release(); scales.release(); zps.release();
+        scales_min.release(); zps_min.release(); scores.release();
+        codes.release(); codes_min.release();
+        sel_blocks.release(); sel_counts.release();
+        part_o.release(); part_ml.release();
+        stage_q.release(); stage_out.release();
+    }
+};
+
+}  // namespace
+
+struct absp_ctx {
+    int device = 0;
+    absp_config cfg{};
+    std::vector<Layer> layers;
+    uint64_t launches = 0;
+};
+
+namespace {
+
+uint32_t G_of(const absp_config& c) { return c.num_q_heads / c.num_kv_heads; }
+uint32_t words_per_centroid(const absp_config& c) { return c.head_dim * c.quant_bits / 32; }
+
+LayerView view_of(absp_ctx* ctx, Layer& l) {
+    const absp_config& c = ctx->cfg;
+    LayerView v{};
+    v.H = c.num_kv_heads;
+    v.G = G_of(c);
+    v.D = c.head_dim;
+    v.P = c.page_size;
+    v.bits = c.quant_bits;
+    v.mode = c.quant_mode;
+    v.method = c.centroid_method;
+    v.batch = l.batch;
+    v.units = uint32_t(l.desc.size());
+    v.max_pages = l.max_pages;
+    v.pool_pages = l.pool_pages;
+    v.k_pool = l.k_pool;
+    v.v_pool = l.v_pool;
+    v.page_table = l.page_table;
+    v.desc = l.d_desc.p;
+    v.values = l.values.p;
+    v.values_min = l.values_min.p;
+    v.codes = l.codes.p;
+    v.codes_min = l.codes_min.p;
+    v.scales = l.scales.p;
+    v.zps = l.zps.p;
+    v.scales_min = l.scales_min.p;
+    v.zps_min = l.zps_min.p;
+    v.scores = l.scores.p;
+    return v;
+}
+
+absp_status get_layer(absp_ctx* ctx, uint32_t layer, Layer** out) {
+    if (!ctx) return fail(ABSP_EINVAL, "null context");
+    if (layer >= ctx->layers.size())
+        return fail(ABSP_ERANGE, "layer " + std::to_string(layer) + " out of range (have " +
+                                     std::to_string(ctx->layers.size()) + ")");
+    *out = &ctx->layers[layer];
+    return ABSP_OK;
+}
+
+// Attention chunks needed for a unit holding `entries` selected blocks.
+uint32_t chunks_for(uint32_t entries, uint32_t block) {
+    const uint32_t e = block >= kAttnChunkRows ? 1u : kAttnChunkRows / block;
+    return ceil_div(entries, e);
+}
+
+}  // namespace
+
+extern "C" {
+
+int absp_abi_version(void) { return ABSP_ABI_VERSION; }
+
+const char* absp_last_error(void) { return g_err.c_str(); }
+
+absp_status absp_config_validate(const absp_config* cfg) {
+    if (!cfg) return fail(ABSP_EINVAL, "null config");
+    const absp_config& c = *cfg;
+    // EngineConfig::validate, config.cpp:48-78 (same order, same messages)
+    if (c.num_kv_heads == 0) return fail(ABSP_EINVAL, "num_heads must be positive");
+    if (c.head_dim == 0) return fail(ABSP_EINVAL, "head_dim must be positive");
+    if (c.page_size == 0) return fail(ABSP_EINVAL, "page_size must be >= 1");
+    if (c.num_candidates == 0 || c.num_candidates > ABSP_MAX_CANDIDATES)
+        return fail(ABSP_EINVAL, "candidate_block_sizes must not be empty");
+    uint32_t maxc = 0;
+    for (uint32_t i = 0; i < c.num_candidates; ++i) {
+        const uint32_t b = c.candidate_block_sizes[i];
+        if (b == 0 || b % c.page_size != 0)
+            return fail(ABSP_EINVAL, "candidate block size " + std::to_string(b) +
+                                         " is not a positive multiple of page_size " +
+                                         std::to_string(c.page_size));
+        maxc = std::max(maxc, b);
+    }
+    for (uint32_t i = 1; i < c.num_candidates; ++i) {
+        if (c.candidate_block_sizes[i] < c.candidate_block_sizes[i - 1])
+            return fail(ABSP_EINVAL, "candidate_block_sizes must be ascending");
+        if (c.candidate_block_sizes[i] == c.candidate_block_sizes[i - 1])
+            return fail(ABSP_EINVAL, "candidate_block_sizes must be distinct");
+    }
+    if (c.token_budget < maxc)
+        return fail(ABSP_EINVAL, "token_budget must be >= the largest candidate block size");
+    if (c.quant_bits != 0 && c.quant_bits != 2 && c.quant_bits != 4 && c.quant_bits != 8)
+        return fail(ABSP_EINVAL, "quant bits must be one of {2, 4, 8}");
+    if (c.quant_mode > 1) return fail(ABSP_EINVAL, "quant mode must be sym (0) or asym (1)");
+    if (c.centroid_method > 1)
+        return fail(ABSP_EINVAL, "unknown centroid method (expected mean|maxmin)");
+    // Extensions and this build's kernel limits.
+    if (c.num_q_heads == 0 || c.num_q_heads % c.num_kv_heads != 0)
+        return fail(ABSP_EINVAL, "num_q_heads must be a positive multiple of num_kv_heads");
+    if (G_of(c) > 8) return fail(ABSP_EINVAL, "GQA group size above 8 is not supported");
+    if (c.head_dim != 64 && c.head_dim != 128)
+        return fail(ABSP_EINVAL, "this build supports head_dim 64 or 128");
+    if (maxc > kAttnChunkRows)
+        return fail(ABSP_EINVAL, "block sizes above 128 are not supported by this build");
+    if (c.max_batch == 0 || c.max_seq_len == 0 || c.num_layers == 0)
+        return fail(ABSP_EINVAL, "max_batch, max_seq_len and num_layers must be positive");
+    const uint32_t minc = c.candidate_block_sizes[0];
+    if (ceil_div(c.token_budget, minc) > 2048)
+        return fail(ABSP_EINVAL, "token_budget / min block size above 2048 is not supported");
+    if (ceil_div(c.max_seq_len, minc) > 131072)
+        return fail(ABSP_EINVAL, "max_seq_len / min block size above 131072 is not supported");
+    return ABSP_OK;
+}
+
+absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) {
+    if (!out) return fail(ABSP_EINVAL, "null output pointer");
+    *out = nullptr;
+    absp_status st = absp_config_validate(cfg);
+    if (st != ABSP_OK) return st;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev)
+        return fail(ABSP_ERANGE, "device " + std::to_string(device) + " out of range");
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(ABSP_ECUDA, "cudaSetDevice failed");
+    cudaDeviceProp prop{};
+    ABSP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(ABSP_ECUDA, "this library is built for sm_100a (B200); device is sm_" +
+                                    std::to_string(prop.major) + std::to_string(prop.minor));
+    ABSP_CUDA(init_attend_attributes());
+    auto* ctx = new absp_ctx;
+    ctx->device = device;
+    ctx->cfg = *cfg;
+    ctx->layers.resize(cfg->num_layers);
+    *out = ctx;
+    return ABSP_OK;
+}
+
+absp_status absp_ctx_destroy(absp_ctx* ctx) {
+    if (!ctx) return ABSP_OK;
+    {
+        DeviceGuard dg(ctx->device);
+        for (Layer& l : ctx->layers) l.release();
+    }
+    delete ctx;
+    return ABSP_OK;
+}
+
+absp_status absp_set_assignment(absp_ctx* ctx, uint32_t layer, const uint32_t* block_sizes) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!block_sizes) return fail(ABSP_EINVAL, "null block_sizes");
+    const absp_config& c = ctx->cfg;
+    // BlockAssignment::validate, centroids.cpp:59-76
+    for (uint32_t h = 0; h < c.num_kv_heads; ++h) {
+        const uint32_t b = block_sizes[h];
+        bool cand = false;
+        for (uint32_t i = 0; i < c.num_candidates; ++i) cand |= c.candidate_block_sizes[i] == b;
+        if (!cand)
+            return fail(ABSP_EINVAL, "head " + std::to_string(h) + ": block size " +
+                                         std::to_string(b) + " is not a candidate");
+        if (b % c.page_size != 0)
+            return fail(ABSP_EINVAL, "head " + std::to_string(h) + ": block size " +
+                                         std::to_string(b) + " is not a multiple of page_size");
+    }
+    l->block_sizes.assign(block_sizes, block_sizes + c.num_kv_heads);
+    l->assigned = true;
+    l->bound = false;
+    l->built = false;
+    return ABSP_OK;
+}
+
+absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, const void* v_pool,
+                         uint64_t pool_pages, const uint32_t* page_table,
+                         uint32_t max_pages_per_seq, const uint32_t* seq_lens, uint32_t batch) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->assigned) return fail(ABSP_ESTATE, "kv_bind: call absp_set_assignment first");
+    const absp_config& c = ctx->cfg;
+    if (!k_pool || !v_pool || !page_table || !seq_lens)
+        return fail(ABSP_EINVAL, "kv_bind: null pointer");
+    if (batch == 0 || batch > c.max_batch)
+        return fail(ABSP_EINVAL, "kv_bind: batch must be in 1..max_batch");
+    if (pool_pages == 0) return fail(ABSP_EINVAL, "kv_bind: pool_pages must be positive");
+    uint32_t max_len = 0;
+    for (uint32_t b = 0; b < batch; ++b) {
+        if (seq_lens[b] == 0)
+            return fail(ABSP_EINVAL, "compute_block_centroids: cache is empty (sequence " +
+                                         std::to_string(b) + ")");
+        if (seq_lens[b] > c.max_seq_len)
+            return fail(ABSP_ECAPACITY, "kv cache at capacity (" + std::to_string(c.max_seq_len) +
+                                            " tokens)");
+        max_len = std::max(max_len, seq_lens[b]);
+    }
+    if (uint64_t(max_pages_per_seq) * c.page_size < max_len)
+        return fail(ABSP_EINVAL, "kv_bind: page table shorter than the longest sequence");
+
+    DeviceGuard dg(ctx->device);
+    if (!dg.ok) return fail(ABSP_ECUDA, "cudaSetDevice failed");
+    l->k_pool = static_cast<const uint16_t*>(k_pool);
+    l->v_pool = static_cast<const uint16_t*>(v_pool);
+    l->pool_pages = pool_pages;
+    l->page_table = page_table;
+    l->max_pages = max_pages_per_seq;
+    l->batch = batch;
+    l->seq_lens.assign(seq_lens, seq_lens + batch);
+
+    // Units, capacity-reserved store segments, score work items.
+    const uint32_t H = c.num_kv_heads;
+    l->desc.clear();
+    l->items.clear();
+    l->total_cap = 0;
+    l->total_centroids = 0;
+    l->max_cap = l->max_nblocks = l->max_budget = l->max_select = l->step_chunks = 0;
+    for (uint32_t b = 0; b < batch; ++b) {
+        for (uint32_t h = 0; h < H; ++h) {
+            UnitDesc d{};
+            d.seq = b;
+            d.head = h;
+            d.block = l->block_sizes[h];
+            d.n_tokens = seq_lens[b];
+            d.n_blocks = ceil_div(d.n_tokens, d.block);
+            d.budget = ceil_div(c.token_budget, d.block);
+            d.cap = ceil_div(c.max_seq_len, d.block);
+            d.seg = l->total_cap;
+            l->total_cap += d.cap;
+            l->total_centroids += d.n_blocks;
+            const uint32_t sel = std::min(d.n_blocks, d.budget);
+            l->max_cap = std::max(l->max_cap, d.cap);
+            l->max_nblocks = std::max(l->max_nblocks, d.n_blocks);
+            l->max_budget = std::max(l->max_budget, d.budget);
+            l->max_select = std::max(l->max_select, sel);
+            l->step_chunks = std::max(l->step_chunks, chunks_for(sel, d.block));
+            const uint32_t u = uint32_t(l->desc.size());
+            for (uint32_t s = 0; s < d.n_blocks; s += kScoreItemCentroids) l->items.push_back({u, s});
+            l->desc.push_back(d);
+        }
+    }
+    const size_t units = l->desc.size();
+    const size_t D = c.head_dim;
+    const bool mm = c.centroid_method == ABSP_CENTROID_MAXMIN;
+    const size_t W = words_per_centroid(c);
+    ABSP_CUDA(l->d_desc.ensure(units));
+    ABSP_CUDA(l->d_items.ensure(l->items.size()));
+    ABSP_CUDA(l->values.ensure(l->total_cap * D));
+    if (mm) ABSP_CUDA(l->values_min.ensure(l->total_cap * D));
+    if (c.quant_bits) {
+        ABSP_CUDA(l->codes.ensure(l->total_cap * W));
+        ABSP_CUDA(l->scales.ensure(units * D));
+        ABSP_CUDA(l->zps.ensure(units * D));
+        if (mm) {
+            ABSP_CUDA(l->codes_min.ensure(l->total_cap * W));
+            ABSP_CUDA(l->scales_min.ensure(units * D));
+            ABSP_CUDA(l->zps_min.ensure(units * D));
+        }
+    }
+    ABSP_CUDA(l->scores.ensure(l->total_cap));
+    l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
+    ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
+    ABSP_CUDA(l->sel_counts.ensure(units));
+    ABSP_CUDA(l->part_o.ensure(units * size_t(l->step_chunks) * 8 * D));
+    ABSP_CUDA(l->part_ml.ensure(units * size_t(l->step_chunks) * 16));
+    ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
+                         cudaMemcpyHostToDevice));
+    l->bound = true;
+    l->built = false;
+    return ABSP_OK;
+}
+
+absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->bound) return fail(ABSP_ESTATE, "build_store: call absp_kv_bind first");
+    DeviceGuard dg(ctx->device);
+    int n = 0;
+    cudaError_t e = launch_build_store(view_of(ctx, *l), l->max_cap, cudaStream_t(stream), &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "build_store kernels");
+    l->built = true;
+    return ABSP_OK;
+}
+
+static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* blocks,
+                             uint32_t stride, uint32_t* counts, cudaStream_t s) {
+    const LayerView v = view_of(ctx, *l);
+    int n = 0;
+    cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), l->d_items.p,
+                                 uint32_t(l->items.size()), s, &n);
+    if (e == cudaSuccess) e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, s, &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "select kernels");
+    return ABSP_OK;
+}
+
+absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* blocks,
+                        uint32_t blocks_stride, uint32_t* counts, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "select: call absp_build_store first");
+    if (!q || !blocks || !counts) return fail(ABSP_EINVAL, "select: null pointer");
+    if (blocks_stride < l->max_select)
+        return fail(ABSP_EINVAL, "select: blocks_stride " + std::to_string(blocks_stride) +
+                                     " < max_select " + std::to_string(l->max_select));
+    DeviceGuard dg(ctx->device);
+    return do_select(ctx, l, q, blocks, blocks_stride, counts, cudaStream_t(stream));
+}
+
+absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint32_t* blocks,
+                        uint32_t blocks_stride, const uint32_t* counts, float* out, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->bound) return fail(ABSP_ESTATE, "attend: call absp_kv_bind first");
+    if (!q || !blocks || !counts || !out) return fail(ABSP_EINVAL, "attend: null pointer");
+    if (blocks_stride == 0) return fail(ABSP_EINVAL, "attend: blocks_stride must be positive");
+    DeviceGuard dg(ctx->device);
+    // A fixed split count (the full-budget chunk count) bounds the grid and the
+    // partial buffers for any selection: splits loop over extra chunks.
+    const uint32_t chunks = std::max(l->step_chunks, 1u);
+    int n = 0;
+    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), blocks,
+                                  blocks_stride, counts, chunks, l->part_o.p, l->part_ml.p, out,
+                                  cudaStream_t(stream), &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
+    return ABSP_OK;
+}
+
+absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
+                             void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "decode_step: call absp_build_store first");
+    if (!q || !out) return fail(ABSP_EINVAL, "decode_step: null pointer");
+    DeviceGuard dg(ctx->device);
+    const cudaStream_t s = cudaStream_t(stream);
+    st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, s);
+    if (st != ABSP_OK) return st;
+    int n = 0;
+    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->sel_blocks.p,
+                                  l->sel_stride, l->sel_counts.p, l->step_chunks, l->part_o.p,
+                                  l->part_ml.p, out, s, &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
+    return ABSP_OK;
+}
+
+absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_host,
+                                  float* out_host, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "decode_step: call absp_build_store first");
+    if (!q_host || !out_host) return fail(ABSP_EINVAL, "decode_step_host: null pointer");
+    DeviceGuard dg(ctx->device);
+    const absp_config& c = ctx->cfg;
+    const size_t nq = size_t(l->batch) * c.num_q_heads * c.head_dim;
+    ABSP_CUDA(l->stage_q.ensure(nq));
+    ABSP_CUDA(l->stage_out.ensure(nq));
+    const cudaStream_t s = cudaStream_t(stream);
+    ABSP_CUDA(cudaMemcpyAsync(l->stage_q.p, q_host, nq * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+    st = absp_decode_step(ctx, layer, l->stage_q.p, l->stage_out.p, stream);
+    if (st != ABSP_OK) return st;
+    ABSP_CUDA(cudaMemcpyAsync(out_host, l->stage_out.p, nq * sizeof(float), cudaMemcpyDeviceToHost, s));
+    ABSP_CUDA(cudaStreamSynchronize(s));
+    return ABSP_OK;
+}
+
+absp_status absp_last_selection(absp_ctx* ctx, uint32_t layer, const uint32_t** blocks,
+                                uint32_t* blocks_stride, const uint32_t** counts) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->bound) return fail(ABSP_ESTATE, "last_selection: layer not bound");
+    if (blocks) *blocks = l->sel_blocks.p;
+    if (blocks_stride) *blocks_stride = l->sel_stride;
+    if (counts) *counts = l->sel_counts.p;
+    return ABSP_OK;
+}
+
+absp_status absp_get_layer_info(absp_ctx* ctx, uint32_t layer, absp_layer_info* info) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!info) return fail(ABSP_EINVAL, "null info");
+    if (!l->bound) return fail(ABSP_ESTATE, "layer_info: layer not bound");
+    const absp_config& c = ctx->cfg;
+    *info = absp_layer_info{};
+    info->batch = l->batch;
+    info->max_select = l->max_select;
+    info->total_centroids = l->total_centroids;
+    const uint64_t W = words_per_centroid(c);
+    const bool mm = c.centroid_method == ABSP_CENTROID_MAXMIN;
+    const uint64_t units = l->desc.size();
+    info->store_bytes = l->total_cap * c.head_dim * 4 * (mm ? 2 : 1) +
+                        (c.quant_bits ? (l->total_cap * W * 4 + units * c.head_dim * 8) * (mm ? 2 : 1) : 0);
+    info->code_bytes = c.quant_bits ? l->total_centroids * c.head_dim * c.quant_bits / 8 * (mm ? 2 : 1)
+                                    : l->total_centroids * c.head_dim * 4 * (mm ? 2 : 1);
+    uint64_t kv = 0;
+    for (const UnitDesc& d : l->desc) {
+        const uint32_t sel = std::min(d.n_blocks, d.budget);
+        // rows attended: all full blocks except possibly the trailing partial one
+        const uint64_t trailing = d.n_tokens - uint64_t(d.n_blocks - 1) * d.block;
+        const uint64_t rows = uint64_t(sel - 1) * d.block + trailing;
+        kv += rows * c.head_dim * 2 * 2;
+    }
+    info->kv_bytes_selected = kv;
+    return ABSP_OK;
+}
+
+absp_status absp_download_store(absp_ctx* ctx, uint32_t layer, uint32_t seq, uint64_t* offsets,
+                                float* values, float* values_min, uint8_t* codes,
+                                uint8_t* codes_min, float* scales, float* zps, float* scales_min,
+                                float* zps_min) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "download_store: store not built");
+    if (seq >= l->batch) return fail(ABSP_ERANGE, "download_store: sequence out of range");
+    DeviceGuard dg(ctx->device);
+    ABSP_CUDA(cudaDeviceSynchronize());
+    const absp_config& c = ctx->cfg;
+    const uint32_t H = c.num_kv_heads, D = c.head_dim, W = words_per_centroid(c);
+    const bool mm = c.centroid_method == ABSP_CENTROID_MAXMIN;
+    uint64_t off = 0;
+    if (offsets) offsets[0] = 0;
+    std::vector<uint32_t> words;
+    for (uint32_t h = 0; h < H; ++h) {
+        const UnitDesc& d = l->desc[size_t(seq) * H + h];
+        const uint32_t u = seq * H + h;
+        const size_t n = d.n_blocks;
+        if (values) ABSP_CUDA(cudaMemcpy(values + off * D, l->values.p + d.seg * D, n * D * 4, cudaMemcpyDeviceToHost));
+        if (values_min && mm)
+            ABSP_CUDA(cudaMemcpy(values_min + off * D, l->values_min.p + d.seg * D, n * D * 4, cudaMemcpyDeviceToHost));
+        if (c.quant_bits) {
+            const int bits = int(c.quant_bits), cpw = 32 / bits;
+            for (int a = 0; a < (mm ? 2 : 1); ++a) {
+                uint8_t* dst = a ? codes_min : codes;
+                if (!dst) continue;
+                const uint32_t* src = (a ? l->codes_min.p : l->codes.p) + d.seg * W;
+                words.resize(size_t(W) * d.cap);
+                ABSP_CUDA(cudaMemcpy(words.data(), src, words.size() * 4, cudaMemcpyDeviceToHost));
+                for (size_t i = 0; i < n; ++i)
+                    for (uint32_t ch = 0; ch < D; ++ch) {
+                        const uint32_t w = words[size_t(ch / cpw) * d.cap + i];
+                        dst[(off + i) * D + ch] = uint8_t((w >> ((ch % cpw) * bits)) & ((1u << bits) - 1u));
+                    }
+            }
+            if (scales) ABSP_CUDA(cudaMemcpy(scales + size_t(h) * D, l->scales.p + size_t(u) * D, D * 4, cudaMemcpyDeviceToHost));
+            if (zps) ABSP_CUDA(cudaMemcpy(zps + size_t(h) * D, l->zps.p + size_t(u) * D, D * 4, cudaMemcpyDeviceToHost));
+            if (mm && scales_min)
+                ABSP_CUDA(cudaMemcpy(scales_min + size_t(h) * D, l->scales_min.p + size_t(u) * D, D * 4, cudaMemcpyDeviceToHost));
+            if (mm && zps_min)
+                ABSP_CUDA(cudaMemcpy(zps_min + size_t(h) * D, l->zps_min.p + size_t(u) * D, D * 4, cudaMemcpyDeviceToHost));
+        }
+        off += n;
+        if (offsets) offsets[h + 1] = off;
+    }
+    return ABSP_OK;
+}
+
+absp_status absp_download_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* scores) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "download_scores: store not built");
+    if (seq >= l->batch) return fail(ABSP_ERANGE, "download_scores: sequence out of range");
+    if (!scores) return fail(ABSP_EINVAL, "null scores");
+    DeviceGuard dg(ctx->device);
+    ABSP_CUDA(cudaDeviceSynchronize());
+    const uint32_t H = ctx->cfg.num_kv_heads;
+    uint64_t off = 0;
+    for (uint32_t h = 0; h < H; ++h) {
+        const UnitDesc& d = l->desc[size_t(seq) * H + h];
+        ABSP_CUDA(cudaMemcpy(scores + off, l->scores.p + d.seg, size_t(d.n_blocks) * 4, cudaMemcpyDeviceToHost));
+        off += d.n_blocks;
+    }
+    return ABSP_OK;
+}
+
+absp_status absp_fill_synthetic_bf16(void* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
+                                     void* stream) {
+    if (!dst && count) return fail(ABSP_EINVAL, "null destination");
+    cudaError_t e = launch_fill_synth(static_cast<uint16_t*>(dst), count, seed, stream_id,
+                                      cudaStream_t(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "fill_synthetic");
+    return ABSP_OK;
+}
+
+uint64_t absp_launch_count(absp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+"""GPU parity: the sm_100a path through the C ABI against the reference's committed
+outputs (tests/golden) and the C restatement (oracle/), on identical bf16 inputs.
+
+  store (centroids, codes, scales, zero points) : bit-exact
+  scores                                        : bit-exact
+  selected block ids (ordered)                  : bit-exact
+  attention output                              : |got-want| <= 1e-3 + 1e-2|want|
+"""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from golden.make_golden import CASES, case_inputs  # noqa: E402
+from layer_data import Layer, make_layer, oracle_step  # noqa: E402
+
+GOLDEN = Path(__file__).parent / "golden" / "golden_v1.npz"
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+def _golden_layer(name) -> tuple:
+    c = case_inputs(name)
+    pages = len(c["page_table"])
+    pt = np.zeros((1, pages + 1), np.uint32)
+    pt[0, :pages] = c["page_table"]
+    layer = Layer(c["H"], c["G"], c["d"], c["P"], c["block_sizes"], [c["n"]], c["k_pool"], c["v_pool"], pt,
+                  c["q"].reshape(1, c["H"] * c["G"], c["d"]))
+    return c, layer
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_golden_cases(cuda, golden, name):
+    from gpu_util import GpuLayer, within_tol
+    c, layer = _golden_layer(name)
+    g = lambda k: golden[f"{name}/{k}"]
+    gl = GpuLayer(layer, c["T"], c["method"], c["bits"], c["mode"])
+    st = gl.da.download_store(0, 0)
+    assert np.array_equal(st["offsets"], g("offsets"))
+    assert np.array_equal(_bits(st["values"]), _bits(g("values")))
+    if c["method"] == 1:
+        assert np.array_equal(_bits(st["values_min"]), _bits(g("values_min")))
+    if c["bits"]:
+        assert np.array_equal(st["codes"], g("codes"))
+        assert np.array_equal(_bits(st["scales"]), _bits(g("scales")))
+        assert np.array_equal(_bits(st["zps"]), _bits(g("zps")))
+        if c["method"] == 1:
+            assert np.array_equal(st["codes_min"], g("codes_min"))
+            assert np.array_equal(_bits(st["scales_min"]), _bits(g("scales_min")))
+    sel = gl.select()[0]
+    assert np.array_equal(_bits(gl.da.download_scores(0, 0)), _bits(g("scores")))
+    assert np.array_equal(np.array([len(s) for s in sel], np.uint32), g("sel_counts"))
+    assert np.array_equal(np.concatenate(sel), g("sel_blocks"))
+    out = gl.decode()[0]
+    ok, err = within_tol(out, g("attn_out"))
+    assert ok, f"max abs err {err}"
+    if c["n"] <= c["T"]:  # full coverage: also within tolerance of the fp64 oracle
+        ok, err = within_tol(out, g("full_out"))
+        assert ok, f"vs full attention: max abs err {err}"
+
+
+@pytest.mark.parametrize("G,H,P,cands,seq_lens,T", [
+    (4, 8, 8, (8, 16, 32), (8192,), 1024),                  # cfg 1 shape (Llama-3.1-8B layer)
+    (4, 8, 16, (16, 32, 64), (5000, 3333, 17, 12000), 2048),  # ragged batch, cfg 3 block sizes
+    (8, 8, 4, (4, 8, 16, 32, 64), (9001, 6000), 2048),        # cfg 5 shape (Qwen3-32B, G=8, P=4)
+    (1, 2, 16, (16,), (700, 64), 128),                        # MHA, uniform blocks
+    (2, 4, 16, (16, 32, 64), (100, 2000), 4096),              # T >= n: every block selected
+])
+def test_random_batches_vs_oracle(cuda, G, H, P, cands, seq_lens, T):
+    from gpu_util import GpuLayer, within_tol
+    layer = make_layer(sum(seq_lens) + G, H=H, G=G, d=128, P=P, block_sizes=cands, seq_lens=seq_lens)
+    gl = GpuLayer(layer, T, 0, 4, 1, max_seq_len=max(seq_lens) + 100)
+    sel = gl.select()
+    out = gl.decode()
+    for b in range(layer.batch):
+        seq, sc, want_sel, want = oracle_step(layer, b, T)
+        st = gl.da.download_store(0, b)
+        assert np.array_equal(st["codes"], seq.codes)
+        assert np.array_equal(_bits(st["scales"]), _bits(seq.scales))
+        assert np.array_equal(_bits(gl.da.download_scores(0, b)), _bits(sc))
+        for h in range(H):
+            assert np.array_equal(sel[b][h], want_sel[h]), (b, h)
+        ok, err = within_tol(out[b], want)
+        assert ok, f"seq {b}: max abs err {err}"
+
+
+@pytest.mark.parametrize("method,bits,mode", [(0, 4, 0), (0, 8, 1), (0, 2, 0), (0, 0, 1), (1, 4, 1), (1, 8, 0), (1, 0, 1)])
+def test_quant_grid_vs_oracle(cuda, method, bits, mode):
+    from gpu_util import GpuLayer
+    layer = make_layer(7 + bits + method, H=8, G=4, d=128, P=16, seq_lens=(3000, 1234), scale=3.0)
+    gl = GpuLayer(layer, 512, method, bits, mode)
+    sel = gl.select()
+    for b in range(layer.batch):
+        seq, sc, want_sel, _ = oracle_step(layer, b, 512, method, bits, mode)
+        st = gl.da.download_store(0, b)
+        assert np.array_equal(_bits(st["values"]), _bits(seq.values))
+        if bits:
+            assert np.array_equal(st["codes"], seq.codes)
+        assert np.array_equal(_bits(gl.da.download_scores(0, b)), _bits(sc))
+        assert all(np.array_equal(x, y) for x, y in zip(sel[b], want_sel))
+
+
+def test_ties_pick_lowest_indices(cuda):
+    from gpu_util import GpuLayer
+    # all keys equal -> all centroids and scores equal -> lowest block ids + trailing block
+    layer = make_layer(3, H=4, G=2, d=64, P=16, seq_lens=(4000,))
+    layer.k_pool[:] = 0x3F80
+    gl = GpuLayer(layer, 256)
+    sel = gl.select()[0]
+    for h, b in enumerate(layer.block_sizes):
+        n_blocks = (4000 + b - 1) // b
+        k = (256 + b - 1) // b
+        assert sel[h].tolist() == list(range(k - 1)) + [n_blocks - 1]
+
+
+def test_block_to_pages_through_attend(cuda):
+    """test_kv_cache.cpp:86-111 through the C ABI: zero keys (uniform weights) and value rows
+    holding their physical page id; block 5 at B=32/P=16 reads pages 10,11 -> 10.5; the
+    trailing block 3 of n=100 reads 4 rows of page 6 -> 6."""
+    from gpu_util import GpuLayer
+    from oracle.oracle import f32_to_bf16
+    P, d, pages = 16, 64, 13
+    vf = np.broadcast_to(np.arange(pages, dtype=np.float32)[None, :, None, None], (1, pages, P, d)).copy()
+    for n, blk, want in ((192, 5, 10.5), (100, 3, 6.0)):
+        layer = make_layer(1, H=1, G=1, d=d, P=P, block_sizes=(32,), seq_lens=(n,))
+        layer.k_pool = np.zeros((1, pages, P, d), np.uint16)
+        layer.v_pool = f32_to_bf16(vf)
+        layer.page_table = np.zeros((1, pages), np.uint32)
+        layer.page_table[0] = np.arange(pages)
+        gl = GpuLayer(layer, 64)
+        out = gl.attend([[np.array([blk], np.uint32)]])
+        assert out[0, 0, 0] == pytest.approx(want, abs=1e-6)
+
+
+def test_error_semantics(cuda):
+    from gpu_util import GpuLayer
+    from paper_2605_12110_b200 import (BlockAssignment, CapacityError, DecodeAttention, EngineConfig,
+                                       InvalidArgument, LogicError, OutOfRange, QuantSpec)
+    cfg = EngineConfig(num_heads=2, head_dim=64, page_size=16, candidate_block_sizes=(16, 32), token_budget=64,
+                       quant=QuantSpec(), max_batch=2, max_seq_len=256)
+    da = DecodeAttention(cfg)
+    with pytest.raises(InvalidArgument):
+        da.set_assignment(0, BlockAssignment([16, 48]))
+    with pytest.raises(OutOfRange):
+        da.set_assignment(1, BlockAssignment([16, 32]))
+    k = torch.zeros(2, 40, 16, 64, dtype=torch.int16, device="cuda")
+    pt = torch.zeros(2, 20, dtype=torch.int32, device="cuda")
+    with pytest.raises(LogicError):
+        da.bind(0, k, k, pt, [100, 100])
+    da.set_assignment(0, BlockAssignment([16, 32]))
+    with pytest.raises(CapacityError):
+        da.bind(0, k, k, pt, [300, 10])
+    with pytest.raises(InvalidArgument):
+        da.bind(0, k, k, pt, [0, 10])
+    da.bind(0, k, k, pt, [100, 10])
+    q = torch.zeros(2, 2, 64, dtype=torch.int16, device="cuda")
+    out = torch.zeros(2, 2, 64, dtype=torch.float32, device="cuda")
+    with pytest.raises(LogicError):
+        da.decode_step(0, q, out)
+    da.build_store(0)
+    da.decode_step(0, q, out)
+    torch.cuda.synchronize()
+    # zero query and zero keys: uniform weights over the selected rows of zero values
+    assert torch.all(out == 0)
+
+
+def test_decode_step_host_matches_device(cuda):
+    from gpu_util import GpuLayer
+    layer = make_layer(11, H=8, G=4, d=128, P=16, seq_lens=(6000, 7000))
+    gl = GpuLayer(layer, 1024)
+    dev = gl.decode()
+    q_host = torch.from_numpy(layer.q.view(np.int16)).pin_memory()
+    out_host = torch.empty(dev.shape, dtype=torch.float32).pin_memory()
+    gl.da.decode_step_host(0, q_host, out_host)
+    assert np.array_equal(out_host.numpy(), dev)
+
+
+def test_synthetic_generator_matches_host_twin(cuda):
+    from oracle.synth import synth_bf16
+    from paper_2605_12110_b200 import fill_synthetic_bf16
+    t = torch.empty(1 << 20, dtype=torch.int16, device="cuda")
+    fill_synthetic_bf16(t, 42, 5)
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy().view(np.uint16), synth_bf16(1 << 20, 42, 5))
+
+
+def test_full_size_128k_sequence(cuda):
+    """Config-3 scale for one sequence (128K tokens, 8 KV heads x G=4, d=128, B in {16,32,64},
+    T=2048): store/scores/selection bit-exact and output in tolerance vs the C oracle."""
+    from gpu_util import GpuLayer, within_tol
+    n = 131072
+    layer = make_layer(128, H=8, G=4, d=128, P=16, block_sizes=(16, 32, 64), seq_lens=(n,), extra_pages=0)
+    gl = GpuLayer(layer, 2048)
+    sel = gl.select()[0]
+    out = gl.decode()[0]
+    seq, sc, want_sel, want = oracle_step(layer, 0, 2048)
+    st = gl.da.download_store(0, 0)
+    assert np.array_equal(st["codes"], seq.codes)
+    assert np.array_equal(_bits(gl.da.download_scores(0, 0)), _bits(sc))
+    for h in range(8):
+        assert np.array_equal(sel[h], want_sel[h])
+    ok, err = within_tol(out, want)
+    assert ok, err
