@@ -22,7 +22,8 @@
 // ldmatrix reads below are bank-conflict free. The GQA group is a dense tile:
 //   S^T = K . Q^T      mma.m16n8k16 (M = 16 KV rows, N = 8 query heads, K = d)
 //   O^T = V^T . P^T    mma.m16n8k16 (M = 16 channels, N = 8 heads, K = rows)
-// with P materialised in shared memory as bf16.
+// with P materialised in shared memory as a bf16 hi/lo pair (two MMAs share the
+// V fragments), so P carries ~16 mantissa bits into the PV product.
 // Accumulation is fp32 throughout; tolerance vs the fp32 reference is
 // 1e-3 abs + 1e-2 rel.
 #include "absp_internal.cuh"
@@ -81,7 +82,7 @@ template <int D>
 struct __align__(16) AttnSmem {
     uint16_t k[kRows * D];
     uint16_t v[kRows * D];
-    uint16_t p[8 * kPStride];
+    uint16_t p[2][8 * kPStride];  // P as bf16 hi + bf16 residual (~16 mantissa bits)
     int64_t row_off[kRows];  // element offset of the row in the pool, -1 = masked
     float red[2][4][8];      // per-warp max / sum per head
 };
@@ -241,8 +242,11 @@ __global__ void __launch_bounds__(kThreads) k_attn(LayerView L, const uint16_t* 
                 const float p1 = rv[mt][1] ? exp2f(fmaf(s[mt][2 + hc], scale_log2, -mnew[hc])) : 0.0f;
                 l_run[hc] += p0 + p1;
                 const int h = 2 * t4 + hc;
-                sm.p[h * kPStride + r0] = f2bf(p0);
-                sm.p[h * kPStride + r0 + 8] = f2bf(p1);
+                const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
+                sm.p[0][h * kPStride + r0] = h0;
+                sm.p[0][h * kPStride + r0 + 8] = h1;
+                sm.p[1][h * kPStride + r0] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
+                sm.p[1][h * kPStride + r0 + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
             }
         }
         cp_async_wait<0>();
@@ -258,9 +262,12 @@ __global__ void __launch_bounds__(kThreads) k_attn(LayerView L, const uint16_t* 
                 const uint32_t ch = cbase / 8 + ((lane >> 3) & 1);
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4_t(v_base + (row * D + ((ch ^ (row & 7)) * 8)) * 2, a0, a1, a2, a3);
-                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.p[g * kPStride + ks * 16 + 2 * t4]);
-                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.p[g * kPStride + ks * 16 + 8 + 2 * t4]);
-                mma_bf16(o[mt], a0, a1, a2, a3, b0, b1);
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                    const uint16_t* pp = sm.p[part] + g * kPStride + ks * 16 + 2 * t4;
+                    mma_bf16(o[mt], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(pp),
+                             *reinterpret_cast<const uint32_t*>(pp + 8));
+                }
             }
         }
     }

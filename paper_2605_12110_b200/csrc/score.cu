@@ -52,6 +52,29 @@ __global__ void __launch_bounds__(kThreads) k_score_tbl(LayerView L, const uint1
 
     const ScoreItem it = items[blockIdx.x];
     const UnitDesc du = L.desc[it.unit];
+    const uint32_t* codes = L.codes + du.seg * W;
+    const uint32_t* codes_lo = MAXMIN ? L.codes_min + du.seg * W : nullptr;
+    float* out = L.scores + du.seg;
+
+    // Issue every code-word load of this thread first (coalesced: one 128 B line per
+    // warp per word), so HBM latency overlaps the table construction below.
+    uint32_t idx[kPerThread];
+    bool ok[kPerThread];
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+        const uint32_t i = it.start + j * kThreads + threadIdx.x;
+        ok[j] = i < du.n_blocks;
+        idx[j] = ok[j] ? i : 0;
+    }
+    uint32_t word[kPerThread][W], wlo[kPerThread][MAXMIN ? W : 1];
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+#pragma unroll
+        for (int j = 0; j < kPerThread; ++j) {
+            word[j][w] = __ldg(codes + size_t(w) * du.cap + idx[j]);
+            if (MAXMIN) wlo[j][w] = __ldg(codes_lo + size_t(w) * du.cap + idx[j]);
+        }
+
     load_query<D>(L, du, q, qs);
     __syncthreads();
     const int mid = (1 << (BITS - 1)) - 1;
@@ -67,37 +90,18 @@ __global__ void __launch_bounds__(kThreads) k_score_tbl(LayerView L, const uint1
     }
     __syncthreads();
 
-    const uint32_t* codes = L.codes + du.seg * W;
-    const uint32_t* codes_lo = MAXMIN ? L.codes_min + du.seg * W : nullptr;
-    float* out = L.scores + du.seg;
-
-    uint32_t idx[kPerThread];
-    bool ok[kPerThread];
-#pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-        const uint32_t i = it.start + j * kThreads + threadIdx.x;
-        ok[j] = i < du.n_blocks;
-        idx[j] = ok[j] ? i : 0;
-    }
     float acc[kPerThread];
 #pragma unroll
     for (int j = 0; j < kPerThread; ++j) acc[j] = 0.0f;
-
-#pragma unroll 2
-    for (int w = 0; w < W; ++w) {
-        uint32_t word[kPerThread], wlo[kPerThread];
 #pragma unroll
-        for (int j = 0; j < kPerThread; ++j) {
-            word[j] = __ldg(codes + size_t(w) * du.cap + idx[j]);
-            if (MAXMIN) wlo[j] = __ldg(codes_lo + size_t(w) * du.cap + idx[j]);
-        }
+    for (int w = 0; w < W; ++w) {
 #pragma unroll
         for (int k = 0; k < CPW; ++k) {
             const float* row = tbl + (w * CPW + k) * LV;
 #pragma unroll
             for (int j = 0; j < kPerThread; ++j) {
-                float p = row[(word[j] >> (k * BITS)) & MASK];
-                if (MAXMIN) p = ref_max(p, row[D * LV + ((wlo[j] >> (k * BITS)) & MASK)]);
+                float p = row[(word[j][w] >> (k * BITS)) & MASK];
+                if (MAXMIN) p = ref_max(p, row[D * LV + ((wlo[j][w] >> (k * BITS)) & MASK)]);
                 acc[j] = __fadd_rn(acc[j], p);
             }
         }

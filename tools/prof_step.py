@@ -1,0 +1,37 @@
+"""Profiling driver: one cfg-3 layer (batch 16, 128K ctx, G=4, int4 store), a few
+eager decode steps. Used under ncu (never for reported numbers)."""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from bench import SEED, WORKLOADS  # noqa: E402
+from paper_2605_12110_b200 import (BlockAssignment, DecodeAttention, EngineConfig, QuantSpec,  # noqa: E402
+                                   fill_synthetic_bf16)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="cfg3")
+ap.add_argument("--steps", type=int, default=4)
+a = ap.parse_args()
+w = WORKLOADS[a.workload]
+B, n, H, G, d, P, T = w["batch"], w["n"], w["H"], w["G"], w["d"], w["P"], w["T"]
+pages = B * ((n + P - 1) // P)
+cfg = EngineConfig(num_heads=H, head_dim=d, page_size=P, candidate_block_sizes=tuple(w["cands"]), token_budget=T,
+                   quant=QuantSpec(4), num_q_heads=H * G, max_batch=B, max_seq_len=n)
+da = DecodeAttention(cfg)
+da.set_assignment(0, BlockAssignment.cycled(H, w["cands"]))
+k = torch.empty(H, pages, P, d, dtype=torch.int16, device="cuda")
+v = torch.empty_like(k)
+q = torch.empty(B, H * G, d, dtype=torch.int16, device="cuda")
+for t, s in ((k, 0), (v, 1), (q, 2)):
+    fill_synthetic_bf16(t, SEED, s)
+pt = torch.arange(pages, dtype=torch.int32, device="cuda").reshape(B, -1)
+da.bind(0, k, v, pt, [n] * B)
+da.build_store(0)
+out = torch.empty(B, H * G, d, dtype=torch.float32, device="cuda")
+for _ in range(a.steps):
+    da.decode_step(0, q, out)
+torch.cuda.synchronize()
+print("ok", out.abs().mean().item())
