@@ -65,10 +65,20 @@ cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreItem*
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, cudaStream_t s,
                         int* launches);
+// Attention work list: all 128-row chunks of all units, unit-major.
+struct AttendWork {
+    const uint32_t* chunk_unit;  // [n_work] unit of each chunk
+    const uint32_t* chunk_base;  // [units + 1] first chunk of each unit
+    uint32_t n_work;             // total chunks
+    uint32_t slots_per_unit;     // partial slots reserved per unit (max chunks of a unit)
+    uint32_t* unit_done;         // [units] completion counters (zero between launches)
+    uint32_t grid;               // persistent CTAs (one per SM)
+};
 cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const uint32_t* blocks,
-                          uint32_t stride, const uint32_t* counts, uint32_t chunks_per_unit,
+                          uint32_t stride, const uint32_t* counts, const AttendWork& work,
                           float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches);
+size_t attend_smem_bytes(uint32_t D, uint32_t P);
 cudaError_t init_attend_attributes();  // per device, once
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);

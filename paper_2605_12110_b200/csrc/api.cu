@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "absp_internal.cuh"
@@ -71,6 +72,17 @@ struct DevBuf {
     }
 };
 
+// Device-side attention work list (see AttendWork).
+struct WorkList {
+    DevBuf<uint32_t> chunk_unit, chunk_base, unit_done;
+    uint32_t n_work = 0, slots = 0;
+    void release() {
+        chunk_unit.release();
+        chunk_base.release();
+        unit_done.release();
+    }
+};
+
 struct Layer {
     bool assigned = false, bound = false, built = false;
     std::vector<uint32_t> block_sizes;
@@ -84,8 +96,10 @@ struct Layer {
     std::vector<UnitDesc> desc;
     std::vector<ScoreItem> items;
     uint64_t total_cap = 0, total_centroids = 0;
-    uint32_t max_cap = 0, max_nblocks = 0, max_budget = 0, max_select = 0, step_chunks = 0;
+    uint32_t max_cap = 0, max_nblocks = 0, max_budget = 0, max_select = 0;
     uint32_t sel_stride = 0;
+    WorkList step_work;                      // decode_step: min(N, K) entries per unit
+    std::map<uint32_t, WorkList> attend_work;  // absp_attend, keyed by blocks_stride
 
     DevBuf<UnitDesc> d_desc;
     DevBuf<ScoreItem> d_items;
@@ -104,6 +118,9 @@ struct Layer {
         sel_blocks.release(); sel_counts.release();
         part_o.release(); part_ml.release();
         stage_q.release(); stage_out.release();
+        step_work.release();
+        for (auto& kv : attend_work) kv.second.release();
+        attend_work.clear();
     }
 };
 
@@ -111,6 +128,7 @@ struct Layer {
 
 struct absp_ctx {
     int device = 0;
+    int num_sms = 148;
     absp_config cfg{};
     std::vector<Layer> layers;
     uint64_t launches = 0;
@@ -164,6 +182,43 @@ absp_status get_layer(absp_ctx* ctx, uint32_t layer, Layer** out) {
 uint32_t chunks_for(uint32_t entries, uint32_t block) {
     const uint32_t e = block >= kAttnChunkRows ? 1u : kAttnChunkRows / block;
     return ceil_div(entries, e);
+}
+
+// Builds the chunk list for units holding at most min(N, cap) entries (cap = K for
+// decode, blocks_stride for explicit selections) and sizes the partial buffers.
+absp_status build_work(Layer& l, uint32_t D, bool decode, uint32_t cap, WorkList& wl) {
+    std::vector<uint32_t> base(l.desc.size() + 1, 0), unit_of;
+    uint32_t slots = 1;
+    for (size_t u = 0; u < l.desc.size(); ++u) {
+        const UnitDesc& d = l.desc[u];
+        const uint32_t entries = std::min(d.n_blocks, decode ? d.budget : cap);
+        const uint32_t ch = std::max(chunks_for(entries, d.block), 1u);
+        base[u + 1] = base[u] + ch;
+        slots = std::max(slots, ch);
+        unit_of.insert(unit_of.end(), ch, uint32_t(u));
+    }
+    wl.n_work = base.back();
+    wl.slots = slots;
+    ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
+    ABSP_CUDA(wl.chunk_base.ensure(base.size()));
+    ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
+    ABSP_CUDA(cudaMemcpy(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4, cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
+    ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(slots) * 8 * D));
+    ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(slots) * 16));
+    return ABSP_OK;
+}
+
+AttendWork work_view(const WorkList& wl, int num_sms) {
+    AttendWork w{};
+    w.chunk_unit = wl.chunk_unit.p;
+    w.chunk_base = wl.chunk_base.p;
+    w.n_work = wl.n_work;
+    w.slots_per_unit = wl.slots;
+    w.unit_done = wl.unit_done.p;
+    w.grid = uint32_t(num_sms);
+    return w;
 }
 
 }  // namespace
@@ -243,6 +298,7 @@ absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) 
     ABSP_CUDA(init_attend_attributes());
     auto* ctx = new absp_ctx;
     ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
     ctx->cfg = *cfg;
     ctx->layers.resize(cfg->num_layers);
     *out = ctx;
@@ -326,7 +382,7 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     l->items.clear();
     l->total_cap = 0;
     l->total_centroids = 0;
-    l->max_cap = l->max_nblocks = l->max_budget = l->max_select = l->step_chunks = 0;
+    l->max_cap = l->max_nblocks = l->max_budget = l->max_select = 0;
     for (uint32_t b = 0; b < batch; ++b) {
         for (uint32_t h = 0; h < H; ++h) {
             UnitDesc d{};
@@ -345,7 +401,6 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
             l->max_nblocks = std::max(l->max_nblocks, d.n_blocks);
             l->max_budget = std::max(l->max_budget, d.budget);
             l->max_select = std::max(l->max_select, sel);
-            l->step_chunks = std::max(l->step_chunks, chunks_for(sel, d.block));
             const uint32_t u = uint32_t(l->desc.size());
             for (uint32_t s = 0; s < d.n_blocks; s += kScoreItemCentroids) l->items.push_back({u, s});
             l->desc.push_back(d);
@@ -373,8 +428,14 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
     ABSP_CUDA(l->sel_counts.ensure(units));
-    ABSP_CUDA(l->part_o.ensure(units * size_t(l->step_chunks) * 8 * D));
-    ABSP_CUDA(l->part_ml.ensure(units * size_t(l->step_chunks) * 16));
+    for (auto& kv : l->attend_work) kv.second.release();
+    l->attend_work.clear();
+    st = build_work(*l, c.head_dim, true, 0, l->step_work);
+    if (st != ABSP_OK) return st;
+    // the explicit-selection work list for the context's own stride is prebuilt so
+    // that absp_attend on decode selections can be graph-captured
+    st = build_work(*l, c.head_dim, false, l->sel_stride, l->attend_work[l->sel_stride]);
+    if (st != ABSP_OK) return st;
     ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
                          cudaMemcpyHostToDevice));
@@ -432,13 +493,18 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     if (!q || !blocks || !counts || !out) return fail(ABSP_EINVAL, "attend: null pointer");
     if (blocks_stride == 0) return fail(ABSP_EINVAL, "attend: blocks_stride must be positive");
     DeviceGuard dg(ctx->device);
-    // A fixed split count (the full-budget chunk count) bounds the grid and the
-    // partial buffers for any selection: splits loop over extra chunks.
-    const uint32_t chunks = std::max(l->step_chunks, 1u);
+    // Work list for selections of up to min(N, blocks_stride) entries per unit;
+    // built once per stride (the first call for a new stride allocates).
+    auto it = l->attend_work.find(blocks_stride);
+    if (it == l->attend_work.end()) {
+        st = build_work(*l, ctx->cfg.head_dim, false, blocks_stride, l->attend_work[blocks_stride]);
+        if (st != ABSP_OK) return st;
+        it = l->attend_work.find(blocks_stride);
+    }
     int n = 0;
     cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), blocks,
-                                  blocks_stride, counts, chunks, l->part_o.p, l->part_ml.p, out,
-                                  cudaStream_t(stream), &n);
+                                  blocks_stride, counts, work_view(it->second, ctx->num_sms),
+                                  l->part_o.p, l->part_ml.p, out, cudaStream_t(stream), &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
@@ -457,8 +523,8 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     if (st != ABSP_OK) return st;
     int n = 0;
     cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->sel_blocks.p,
-                                  l->sel_stride, l->sel_counts.p, l->step_chunks, l->part_o.p,
-                                  l->part_ml.p, out, s, &n);
+                                  l->sel_stride, l->sel_counts.p, work_view(l->step_work, ctx->num_sms),
+                                  l->part_o.p, l->part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;

@@ -1,5 +1,5 @@
 // Kernel 3: variable-block-size sparse paged flash-decoding with split-KV
-// partials and a log-sum-exp merge (sm_100a).
+// partials and a fused log-sum-exp merge (sm_100a).
 //
 // Reference: sparse_attention / attend_rows (engine.cpp:180-210, 285-327):
 // softmax(q . k / sqrt(d)) . v over the rows of the selected blocks, rows
@@ -8,24 +8,29 @@
 // index arithmetic: block j of head h covers page-table entries
 // [j*B/P, (j+1)*B/P) — no gather copy, no per-step allocation.
 //
-// Work decomposition: unit u = (b, h) owns its G query heads and its selection.
-// The selection list is cut into chunks of E = 128/B consecutive entries
-// (<= 128 rows). A grid of (nsplit, units) 128-thread CTAs walks the chunks
-// (split s takes chunks s, s+nsplit, ...) with an online softmax, and writes an
-// unnormalised partial (m, l, o[G][d]); k_merge combines the splits of a unit
-// with the usual LSE rescaling. For a full-budget decode step nsplit equals the
-// chunk count, so every CTA handles exactly one chunk.
+// Work: the selection of unit u = (b, h) is cut into chunks of E = 128/B
+// consecutive entries (<= 128 rows = 128/P whole pages). All chunks of all units
+// form one list; a persistent grid (one CTA per SM) takes contiguous ranges of it,
+// so every SM streams the same number of KV bytes regardless of block sizes.
 //
-// Inside a chunk: all K and V rows are requested at once with 16-byte
-// cp.async (zero-filled for rows past the sequence end), written into an
-// XOR-swizzled tile (16 B chunk c of row r stored at c ^ (r & 7)) so the
-// ldmatrix reads below are bank-conflict free. The GQA group is a dense tile:
-//   S^T = K . Q^T      mma.m16n8k16 (M = 16 KV rows, N = 8 query heads, K = d)
-//   O^T = V^T . P^T    mma.m16n8k16 (M = 16 channels, N = 8 heads, K = rows)
-// with P materialised in shared memory as a bf16 hi/lo pair (two MMAs share the
-// V fragments), so P carries ~16 mantissa bits into the PV product.
-// Accumulation is fp32 throughout; tolerance vs the fp32 reference is
-// 1e-3 abs + 1e-2 rel.
+// CTA = 4 consumer warps + 1 producer warp, 3-stage mbarrier ring:
+//   producer : lane s resolves page slot s of the next chunk (selected block ->
+//              page table -> pool page) and issues one cp.async.bulk per page for K
+//              and V (the TMA bulk-copy engine; 1 instruction per 1-4 KB page),
+//              completing on the stage's full barrier.
+//   consumers: S^T = K Q^T and O^T += V^T P^T on mma.m16n8k16 (M = 16 KV rows or
+//              channels, N = 8 query heads of the GQA group), fp32 online softmax
+//              across the chunks of a unit, P kept as a bf16 hi/lo pair (~16
+//              mantissa bits). A run of chunks of one unit ends in a partial
+//              (m, l, o[G][d]); the CTA that completes a unit's last chunk merges
+//              the unit's partials (fused LSE merge, completion counter per unit).
+//
+// Bank conflicts without TMA swizzle: a page lands contiguously in smem, so rows
+// of one page are 256 B apart (same banks). Page slots are therefore staggered by
+// 16 B and logical row i of a chunk is (slot i % NS, row i / NS), NS = 128/P: the
+// 8 rows of every ldmatrix phase come from 8 different slots and hit 8 distinct
+// 16 B bank groups (for P <= 16). Softmax is permutation-invariant over rows, and
+// the same permutation indexes P, so the result is unchanged.
 #include "absp_internal.cuh"
 
 #include <math.h>
@@ -34,21 +39,43 @@ namespace absp {
 namespace {
 
 constexpr int kRows = kAttnChunkRows;  // 128
-constexpr int kThreads = 128;
+constexpr int kConsumers = 128;        // 4 warps
+constexpr int kThreads = kConsumers + 32;
+constexpr int kStages = 3;
 constexpr int kPStride = kRows + 8;    // bf16 row stride of P (bank-conflict free)
+constexpr int kMaxSlots = kRows;       // P >= 1
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
-                 "r"(src_bytes));
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory");
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
@@ -78,299 +105,391 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
     return uint16_t(u >> 16);
 }
 
-template <int D>
-struct __align__(16) AttnSmem {
-    uint16_t k[kRows * D];
-    uint16_t v[kRows * D];
-    uint16_t p[2][8 * kPStride];  // P as bf16 hi + bf16 residual (~16 mantissa bits)
-    int64_t row_off[kRows];  // element offset of the row in the pool, -1 = masked
-    float red[2][4][8];      // per-warp max / sum per head
+struct StageMeta {
+    uint32_t unit;
+    uint32_t chunk;
+    uint32_t any_invalid;       // some row of the chunk carries no token
+    uint16_t valid[kMaxSlots];  // valid rows per page slot (0..P)
 };
 
-template <int D>
-__global__ void __launch_bounds__(kThreads) k_attn(LayerView L, const uint16_t* __restrict__ q,
-                                                   const uint32_t* __restrict__ blocks,
-                                                   uint32_t stride,
-                                                   const uint32_t* __restrict__ counts,
-                                                   float* __restrict__ part_o,
-                                                   float* __restrict__ part_ml) {
-    constexpr int CPR = D / 8;  // 16 B chunks per row
-    constexpr int MT = D / 64;  // 16-channel PV m-tiles per warp
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    AttnSmem<D>& sm = *reinterpret_cast<AttnSmem<D>*>(smem_raw);
+struct SmemHead {  // fixed-size part after the stage tiles
+    unsigned long long full[kStages];
+    unsigned long long empty[kStages];
+    StageMeta meta[kStages];
+    uint16_t p[2][8 * kPStride];  // P as bf16 hi + bf16 residual
+    float red[2][4][8];
+    uint32_t flag;
+};
 
-    const uint32_t u = blockIdx.y;
-    const uint32_t split = blockIdx.x;
-    const uint32_t nsplit = gridDim.x;
-    const UnitDesc du = L.desc[u];
-    const uint32_t B = du.block;
-    const uint32_t E = B >= kRows ? 1u : kRows / B;  // selection entries per chunk
-    const uint32_t cnt = counts[u];
-    const uint32_t G = L.G;
-    float* ml = part_ml + (size_t(u) * nsplit + split) * 16;
-    if (split * E >= cnt) {  // no chunk for this split: neutral partial
-        if (threadIdx.x < 8) {
-            ml[threadIdx.x * 2] = -INFINITY;
-            ml[threadIdx.x * 2 + 1] = 0.0f;
+__host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
+    return ((kRows * D * 2 + (kRows / P) * 16) + 127) / 128 * 128;
+}
+
+// CTA c owns work items [c*W/C, (c+1)*W/C).
+__device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t C) {
+    return uint32_t((uint64_t(c) * W) / C);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
+                                                      const uint32_t* __restrict__ blocks,
+                                                      uint32_t stride,
+                                                      const uint32_t* __restrict__ counts,
+                                                      const uint32_t* __restrict__ chunk_unit,
+                                                      const uint32_t* __restrict__ chunk_base,
+                                                      uint32_t n_work, uint32_t slots_per_unit,
+                                                      float* __restrict__ part_o,
+                                                      float* __restrict__ part_ml,
+                                                      uint32_t* __restrict__ unit_done,
+                                                      float* __restrict__ out) {
+    constexpr int MT = D / 64;  // 16-channel PV m-tiles per consumer warp
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const uint32_t P = L.P;
+    const uint32_t NS = kRows / P;  // page slots per chunk
+    const uint32_t TB = tile_bytes(D, P);
+    const uint32_t slot_stride = P * D * 2 + 16;
+    SmemHead& sh = *reinterpret_cast<SmemHead*>(smem + kStages * 2 * TB);
+    const uint32_t smem_base = smem_u32(smem);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t w_begin = range_begin(blockIdx.x, n_work, gridDim.x);
+    const uint32_t w_end = range_begin(blockIdx.x + 1, n_work, gridDim.x);
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(smem_u32(&sh.full[s]), 1);
+            mbar_init(smem_u32(&sh.empty[s]), kConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kConsumers / 32) {
+        // ============================ producer ================================
+        uint32_t stage = 0, phase = 0;
+        for (uint32_t w = w_begin; w < w_end; ++w) {
+            mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
+            const uint32_t u = chunk_unit[w];
+            const uint32_t c = w - chunk_base[u];
+            const UnitDesc du = L.desc[u];
+            const uint32_t B = du.block;
+            const uint32_t E = kRows / B;
+            const uint32_t ppb = B / P;  // pages per block
+            const uint32_t cnt = counts[u];
+            const uint32_t j0 = c * E;
+            const uint32_t ne = j0 < cnt ? min(E, cnt - j0) : 0u;
+            StageMeta& mt = sh.meta[stage];
+            const uint32_t kdst = smem_base + stage * 2 * TB;
+            const uint32_t full = smem_u32(&sh.full[stage]);
+            const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+            // pass 1: lane = page slot; which slots hold tokens, how many bytes
+            uint32_t bytes = 0, invalid = 0;
+            for (uint32_t s0 = 0; s0 < NS; s0 += 32) {
+                const uint32_t s = s0 + lane;
+                uint32_t valid = 0;
+                if (s < NS) {
+                    const uint32_t e = s / ppb, pp = s % ppb;
+                    if (e < ne) {
+                        const uint32_t t0 = __ldg(blocks + size_t(u) * stride + j0 + e) * B + pp * P;
+                        if (t0 < du.n_tokens) valid = min(P, du.n_tokens - t0);
+                    }
+                    mt.valid[s] = uint16_t(valid);
+                }
+                bytes += __reduce_add_sync(0xffffffffu, valid ? 2 * P * D * 2 : 0u);
+                invalid |= __ballot_sync(0xffffffffu, s < NS && valid < P);
+            }
+            if (lane == 0) {
+                mt.unit = u;
+                mt.chunk = c;
+                mt.any_invalid = invalid ? 1u : 0u;
+                mbar_expect_tx(full, bytes);
+            }
+            __syncwarp();
+            // pass 2: issue the copies (slot lookups re-read from L1)
+            for (uint32_t s0 = 0; s0 < NS; s0 += 32) {
+                const uint32_t s = s0 + lane;
+                if (s < NS && mt.valid[s]) {
+                    const uint32_t e = s / ppb, pp = s % ppb;
+                    const uint32_t blk = __ldg(blocks + size_t(u) * stride + j0 + e);
+                    const uint32_t t0 = blk * B + pp * P;
+                    const uint32_t page = __ldg(pt + t0 / P);
+                    const size_t off = (size_t(du.head) * L.pool_pages + page) * P * D;
+                    bulk_g2s(kdst + s * slot_stride, L.k_pool + off, P * D * 2, full);
+                    bulk_g2s(kdst + TB + s * slot_stride, L.v_pool + off, P * D * 2, full);
+                }
+            }
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
+            }
         }
         return;
     }
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // ============================== consumers =================================
     const uint32_t g = lane >> 2, t4 = lane & 3;
-    const uint32_t k_base = smem_u32(sm.k), v_base = smem_u32(sm.v);
+    const uint32_t G = L.G;
     const float scale_log2 = rsqrtf(float(D)) * 1.4426950408889634f;
-
-    // Q^T fragments (B operand of S^T = K Q^T): b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]
-    uint32_t qb[D / 16][2];
-    {
-        const uint16_t* qrow = q + (size_t(du.seq) * L.H * G + size_t(du.head) * G + g) * D;
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-            qb[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
-            qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
-        }
-    }
-
-    // running state for this thread's head columns h = 2*t4 + {0,1}
-    float m_run[2] = {-INFINITY, -INFINITY};  // log2-scaled running max (block-uniform per head)
-    float l_run[2] = {0.0f, 0.0f};            // this thread's share of the denominators
+    uint32_t stage = 0, phase = 0;
+    uint32_t cur_u = 0xffffffffu, seg_first = 0, seg_last = 0;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     float o[MT][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.0f;
+    uint32_t qb[D / 16][2];
 
-    for (uint32_t chunk = split; chunk * E < cnt; chunk += nsplit) {
-        const uint32_t j0 = chunk * E;
-        const uint32_t ne = min(E, cnt - j0);
-        __syncthreads();  // previous chunk's smem reads are done
-        {   // row table: pool element offset of each of the kRows rows (-1 = masked)
-            const uint32_t r = tid;
-            int64_t off = -1;
-            const uint32_t e = r / B, w = r % B;
-            if (e < ne) {
-                const uint32_t blk = blocks[size_t(u) * stride + j0 + e];
-                const uint32_t t = blk * B + w;
-                if (t < du.n_tokens) {
-                    const uint32_t page = L.page_table[size_t(du.seq) * L.max_pages + t / L.P];
-                    off = int64_t(((size_t(du.head) * L.pool_pages + page) * L.P + t % L.P) * D);
-                }
-            }
-            sm.row_off[r] = off;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (uint32_t idx = tid; idx < kRows * CPR; idx += kThreads) {
-            const uint32_t r = idx / CPR, c = idx % CPR;
-            const int64_t off = sm.row_off[r];
-            cp_async16(k_base + (r * D + ((c ^ (r & 7)) * 8)) * 2, L.k_pool + (off < 0 ? 0 : off) + c * 8,
-                       off < 0 ? 0u : 16u);
-        }
-        cp_async_commit();
-#pragma unroll 4
-        for (uint32_t idx = tid; idx < kRows * CPR; idx += kThreads) {
-            const uint32_t r = idx / CPR, c = idx % CPR;
-            const int64_t off = sm.row_off[r];
-            cp_async16(v_base + (r * D + ((c ^ (r & 7)) * 8)) * 2, L.v_pool + (off < 0 ? 0 : off) + c * 8,
-                       off < 0 ? 0u : 16u);
-        }
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+    // logical row i of a chunk -> byte offset inside a tile
+    auto row_off = [&](uint32_t i) -> uint32_t { return (i % NS) * slot_stride + (i / NS) * (D * 2); };
 
-        // S^T = K Q^T: warp w owns rows [32w, 32w+32)
-        float s[2][4];
+    // Emit the partial of (cur_u, chunks seg_first..seg_last); the CTA completing the
+    // unit merges all of its partials into `out`.
+    auto flush = [&]() {
+        float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            s[mt][0] = s[mt][1] = s[mt][2] = s[mt][3] = 0.0f;
-            const uint32_t row = warp * 32 + mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                const uint32_t ch = ks * 2 + (lane >> 4);
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4(k_base + (row * D + ((ch ^ (row & 7)) * 8)) * 2, a0, a1, a2, a3);
-                mma_bf16(s[mt], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-            }
+            for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
+        consumer_sync();  // red[] free
+        if (g == 0) {
+            sh.red[1][warp][2 * t4] = lsum[0];
+            sh.red[1][warp][2 * t4 + 1] = lsum[1];
         }
-        // this thread's rows: 32w + 16mt + g (+8); heads 2t4, 2t4+1
-        bool rv[2][2];
+        const size_t slot = size_t(cur_u) * slots_per_unit + seg_first;
+        float* po = part_o + slot * 8 * D;
+        float* ml = part_ml + slot * 16;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            rv[mt][0] = sm.row_off[warp * 32 + mt * 16 + g] >= 0;
-            rv[mt][1] = sm.row_off[warp * 32 + mt * 16 + g + 8] >= 0;
-        }
-        float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MT; ++mt) {
+            const uint32_t c0 = warp * (D / 4) + mt * 16 + g;
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
-                if (rv[mt][0]) mx[hc] = fmaxf(mx[hc], s[mt][hc]);
-                if (rv[mt][1]) mx[hc] = fmaxf(mx[hc], s[mt][2 + hc]);
+                const uint32_t h = 2 * t4 + hc;
+                if (h < G) {
+                    po[h * D + c0] = o[mt][hc];
+                    po[h * D + c0 + 8] = o[mt][2 + hc];
+                }
+            }
+        }
+        if (warp == 0 && g == 0) {  // m is block-uniform per head
+            ml[(2 * t4) * 2] = m_run[0];
+            ml[(2 * t4 + 1) * 2] = m_run[1];
+        }
+        consumer_sync();
+        if (tid < 8)
+            ml[tid * 2 + 1] = sh.red[1][0][tid] + sh.red[1][1][tid] + sh.red[1][2][tid] + sh.red[1][3][tid];
+        // chunks of this run after the first carry no partial of their own
+        for (uint32_t c = seg_first + 1 + tid / 8; c <= seg_last; c += kConsumers / 8) {
+            float* mc = part_ml + (size_t(cur_u) * slots_per_unit + c) * 16;
+            mc[(tid % 8) * 2] = -INFINITY;
+            mc[(tid % 8) * 2 + 1] = 0.0f;
+        }
+        // ---- completion counting; the last contributor merges ------------------
+        __threadfence();
+        consumer_sync();
+        const uint32_t total = chunk_base[cur_u + 1] - chunk_base[cur_u];
+        if (tid == 0) {
+            const uint32_t mine = seg_last - seg_first + 1;
+            const uint32_t done = atomicAdd(unit_done + cur_u, mine) + mine;
+            sh.flag = done == total ? 1u : 0u;
+            if (done == total) unit_done[cur_u] = 0u;  // re-arm for the next step
+        }
+        consumer_sync();
+        if (sh.flag) {
+            __threadfence();
+            const UnitDesc du = L.desc[cur_u];
+            const float* mlu = part_ml + size_t(cur_u) * slots_per_unit * 16;
+            for (uint32_t h = warp; h < G; h += kConsumers / 32) {
+                float M = -INFINITY;
+                for (uint32_t c = lane; c < total; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+                constexpr int PER = D / 32;
+                float acc[PER];
+#pragma unroll
+                for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
+                float lsum2 = 0.0f;
+                for (uint32_t c = 0; c < total; ++c) {
+                    const float m = __ldcg(mlu + c * 16 + h * 2);
+                    if (m == -INFINITY) continue;
+                    const float wgt = exp2f(m - M);
+                    lsum2 += wgt * __ldcg(mlu + c * 16 + h * 2 + 1);
+                    const float* pc = part_o + ((size_t(cur_u) * slots_per_unit + c) * 8 + h) * D;
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) acc[i] += wgt * __ldcg(pc + lane + 32 * i);
+                }
+                const float inv = 1.0f / lsum2;
+                float* dst = out + (size_t(du.seq) * L.H * G + size_t(du.head) * G + h) * D;
+#pragma unroll
+                for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
+            }
+        }
+    };
+
+    for (uint32_t w = w_begin; w < w_end; ++w) {
+        mbar_wait(smem_u32(&sh.full[stage]), phase);
+        const StageMeta& mt = sh.meta[stage];
+        const uint32_t u = mt.unit;
+        if (u != cur_u) {
+            if (cur_u != 0xffffffffu) flush();
+            cur_u = u;
+            seg_first = mt.chunk;
+            m_run[0] = m_run[1] = -INFINITY;
+            l_run[0] = l_run[1] = 0.0f;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
+            const UnitDesc du = L.desc[u];
+            const uint16_t* qrow = q + (size_t(du.seq) * L.H * G + size_t(du.head) * G + g) * D;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                qb[ks][0] = g < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4)) : 0u;
+                qb[ks][1] = g < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4)) : 0u;
+            }
+        }
+        seg_last = mt.chunk;
+        const uint32_t k_base = smem_base + stage * 2 * TB;
+        const uint32_t v_base = k_base + TB;
+        const bool any_invalid = mt.any_invalid != 0;
+        if (any_invalid) {
+            // zero the V rows that carry no token: stale or uninitialised smem could
+            // hold NaN/Inf, and 0 * NaN would poison the PV product
+            for (uint32_t i = tid; i < kRows * (D / 8); i += kConsumers) {
+                const uint32_t row = i / (D / 8), ch = i % (D / 8);
+                if ((row / NS) >= mt.valid[row % NS]) {
+                    unsigned char* p = smem + stage * 2 * TB + TB + row_off(row) + ch * 16;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+                }
+            }
+        }
+
+        // S^T = K Q^T: warp w owns logical rows [32w, 32w+32)
+        float s[2][4];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            s[m][0] = s[m][1] = s[m][2] = s[m][3] = 0.0f;
+            const uint32_t row = warp * 32 + m * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+            const uint32_t ra = k_base + row_off(row);
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(ra + (ks * 2 + (lane >> 4)) * 16, a0, a1, a2, a3);
+                mma_bf16(s[m], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+            }
+        }
+        bool rv[2][2];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const uint32_t row = warp * 32 + m * 16 + g + hh * 8;
+                rv[m][hh] = !any_invalid || (row / NS) < mt.valid[row % NS];
+            }
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int hc = 0; hc < 2; ++hc) {
+                if (rv[m][0]) mx[hc] = fmaxf(mx[hc], s[m][hc]);
+                if (rv[m][1]) mx[hc] = fmaxf(mx[hc], s[m][2 + hc]);
             }
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
-            for (int off = 4; off < 32; off <<= 1)
-                mx[hc] = fmaxf(mx[hc], __shfl_xor_sync(0xffffffffu, mx[hc], off));
+            for (int off = 4; off < 32; off <<= 1) mx[hc] = fmaxf(mx[hc], __shfl_xor_sync(0xffffffffu, mx[hc], off));
         if (g == 0) {
-            sm.red[0][warp][2 * t4] = mx[0];
-            sm.red[0][warp][2 * t4 + 1] = mx[1];
+            sh.red[0][warp][2 * t4] = mx[0];
+            sh.red[0][warp][2 * t4 + 1] = mx[1];
         }
-        __syncthreads();
-        float mnew[2], alpha[2];
+        consumer_sync();
+        float mnew[2];
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc) {
             const int h = 2 * t4 + hc;
-            const float cm = fmaxf(fmaxf(sm.red[0][0][h], sm.red[0][1][h]),
-                                   fmaxf(sm.red[0][2][h], sm.red[0][3][h]));
+            const float cm = fmaxf(fmaxf(sh.red[0][0][h], sh.red[0][1][h]), fmaxf(sh.red[0][2][h], sh.red[0][3][h]));
             mnew[hc] = fmaxf(m_run[hc], cm * scale_log2);
-            alpha[hc] = mnew[hc] == -INFINITY ? 1.0f : exp2f(m_run[hc] - mnew[hc]);
+            const float alpha = mnew[hc] == -INFINITY ? 1.0f : exp2f(m_run[hc] - mnew[hc]);
             m_run[hc] = mnew[hc];
-            l_run[hc] *= alpha[hc];
+            l_run[hc] *= alpha;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                o[m][hc] *= alpha;
+                o[m][2 + hc] *= alpha;
+            }
         }
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            o[mt][0] *= alpha[0];
-            o[mt][1] *= alpha[1];
-            o[mt][2] *= alpha[0];
-            o[mt][3] *= alpha[1];
-        }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            const uint32_t r0 = warp * 32 + mt * 16 + g;
+        for (int m = 0; m < 2; ++m) {
+            const uint32_t r0 = warp * 32 + m * 16 + g;
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
-                const float p0 = rv[mt][0] ? exp2f(fmaf(s[mt][hc], scale_log2, -mnew[hc])) : 0.0f;
-                const float p1 = rv[mt][1] ? exp2f(fmaf(s[mt][2 + hc], scale_log2, -mnew[hc])) : 0.0f;
+                const float p0 = rv[m][0] ? exp2f(fmaf(s[m][hc], scale_log2, -mnew[hc])) : 0.0f;
+                const float p1 = rv[m][1] ? exp2f(fmaf(s[m][2 + hc], scale_log2, -mnew[hc])) : 0.0f;
                 l_run[hc] += p0 + p1;
                 const int h = 2 * t4 + hc;
                 const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
-                sm.p[0][h * kPStride + r0] = h0;
-                sm.p[0][h * kPStride + r0 + 8] = h1;
-                sm.p[1][h * kPStride + r0] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
-                sm.p[1][h * kPStride + r0 + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
+                sh.p[0][h * kPStride + r0] = h0;
+                sh.p[0][h * kPStride + r0 + 8] = h1;
+                sh.p[1][h * kPStride + r0] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
+                sh.p[1][h * kPStride + r0 + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
             }
         }
-        cp_async_wait<0>();
-        __syncthreads();
+        consumer_sync();
 
         // O^T += V^T P^T: warp w owns channels [w*D/4, (w+1)*D/4)
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            const uint32_t cbase = warp * (D / 4) + mt * 16;
+        for (int m = 0; m < MT; ++m) {
+            const uint32_t cbase = warp * (D / 4) + m * 16;
 #pragma unroll
             for (int ks = 0; ks < kRows / 16; ++ks) {
                 const uint32_t row = ks * 16 + (lane & 7) + ((lane >> 4) & 1) * 8;
                 const uint32_t ch = cbase / 8 + ((lane >> 3) & 1);
                 uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(v_base + (row * D + ((ch ^ (row & 7)) * 8)) * 2, a0, a1, a2, a3);
+                ldsm_x4_t(v_base + row_off(row) + ch * 16, a0, a1, a2, a3);
 #pragma unroll
                 for (int part = 0; part < 2; ++part) {
-                    const uint16_t* pp = sm.p[part] + g * kPStride + ks * 16 + 2 * t4;
-                    mma_bf16(o[mt], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(pp),
+                    const uint16_t* pp = sh.p[part] + g * kPStride + ks * 16 + 2 * t4;
+                    mma_bf16(o[m], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(pp),
                              *reinterpret_cast<const uint32_t*>(pp + 8));
                 }
             }
         }
-    }
-
-    // ---- partial (m, l, o) of this split ------------------------------------
-#pragma unroll
-    for (int hc = 0; hc < 2; ++hc)
-#pragma unroll
-        for (int off = 4; off < 32; off <<= 1) l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], off);
-    __syncthreads();
-    if (g == 0) {
-        sm.red[1][warp][2 * t4] = l_run[0];
-        sm.red[1][warp][2 * t4 + 1] = l_run[1];
-        if (warp == 0) {
-            sm.red[0][0][2 * t4] = m_run[0];
-            sm.red[0][0][2 * t4 + 1] = m_run[1];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
+        if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
         }
     }
-    float* po = part_o + (size_t(u) * nsplit + split) * 8 * D;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-        const uint32_t c0 = warp * (D / 4) + mt * 16 + g;
-#pragma unroll
-        for (int hc = 0; hc < 2; ++hc) {
-            const uint32_t h = 2 * t4 + hc;
-            if (h < G) {
-                po[h * D + c0] = o[mt][hc];
-                po[h * D + c0 + 8] = o[mt][2 + hc];
-            }
-        }
-    }
-    __syncthreads();
-    if (tid < 8) {
-        const int h = tid;
-        ml[h * 2] = sm.red[0][0][h];
-        ml[h * 2 + 1] = sm.red[1][0][h] + sm.red[1][1][h] + sm.red[1][2][h] + sm.red[1][3][h];
-    }
-}
-
-// LSE merge of the chunk partials of one unit: one warp per query head.
-template <int D>
-__global__ void __launch_bounds__(256) k_merge(LayerView L, uint32_t nchunks,
-                                               const float* __restrict__ part_o,
-                                               const float* __restrict__ part_ml,
-                                               float* __restrict__ out) {
-    const uint32_t u = blockIdx.x;
-    const uint32_t h = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (h >= L.G) return;
-    const UnitDesc du = L.desc[u];
-    const float* ml = part_ml + size_t(u) * nchunks * 16;
-    float M = -INFINITY;
-    for (uint32_t c = 0; c < nchunks; ++c) M = fmaxf(M, ml[c * 16 + h * 2]);
-    constexpr int PER = D / 32;
-    float acc[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
-    float lsum = 0.0f;
-    for (uint32_t c = 0; c < nchunks; ++c) {
-        const float m = ml[c * 16 + h * 2];
-        if (m == -INFINITY) continue;
-        const float w = exp2f(m - M);
-        lsum += w * ml[c * 16 + h * 2 + 1];
-        const float* po = part_o + ((size_t(u) * nchunks + c) * 8 + h) * D;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) acc[i] += w * po[lane + 32 * i];
-    }
-    const float inv = 1.0f / lsum;
-    float* dst = out + (size_t(du.seq) * L.H * L.G + size_t(du.head) * L.G + h) * D;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
-}
-
-template <int D>
-cudaError_t attend_d(const LayerView& L, const uint16_t* q, const uint32_t* blocks,
-                     uint32_t stride, const uint32_t* counts, uint32_t chunks, float* part_o,
-                     float* part_ml, float* out, cudaStream_t s, int* launches) {
-    const size_t smem = sizeof(AttnSmem<D>);
-    k_attn<D><<<dim3(chunks, L.units), kThreads, smem, s>>>(L, q, blocks, stride, counts, part_o,
-                                                            part_ml);
-    k_merge<D><<<L.units, 256, 0, s>>>(L, chunks, part_o, part_ml, out);
-    *launches += 2;
-    return cudaGetLastError();
+    if (cur_u != 0xffffffffu) flush();
 }
 
 }  // namespace
 
+size_t attend_smem_bytes(uint32_t D, uint32_t P) {
+    return size_t(kStages) * 2 * tile_bytes(D, P) + sizeof(SmemHead);
+}
+
 cudaError_t init_attend_attributes() {
+    // the largest footprint over supported (D, P): P = 1 has the most page slots
     cudaError_t e = cudaFuncSetAttribute(k_attn<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sizeof(AttnSmem<64>)));
+                                         int(attend_smem_bytes(64, 1)));
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_attn<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(sizeof(AttnSmem<128>)));
+                                int(attend_smem_bytes(128, 1)));
 }
 
 cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const uint32_t* blocks,
-                          uint32_t stride, const uint32_t* counts, uint32_t chunks_per_unit,
+                          uint32_t stride, const uint32_t* counts, const AttendWork& wk,
                           float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches) {
+    const size_t smem = attend_smem_bytes(L.D, L.P);
+    const uint32_t grid = wk.n_work < wk.grid ? wk.n_work : wk.grid;
+    if (grid == 0) return cudaSuccess;
     if (L.D == 64)
-        return attend_d<64>(L, q, blocks, stride, counts, chunks_per_unit, part_o, part_ml, out, s,
-                            launches);
-    return attend_d<128>(L, q, blocks, stride, counts, chunks_per_unit, part_o, part_ml, out, s,
-                         launches);
+        k_attn<64><<<grid, kThreads, smem, s>>>(L, q, blocks, stride, counts, wk.chunk_unit, wk.chunk_base,
+                                                wk.n_work, wk.slots_per_unit, part_o, part_ml, wk.unit_done,
+                                                out);
+    else
+        k_attn<128><<<grid, kThreads, smem, s>>>(L, q, blocks, stride, counts, wk.chunk_unit, wk.chunk_base,
+                                                 wk.n_work, wk.slots_per_unit, part_o, part_ml, wk.unit_done,
+                                                 out);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 }  // namespace absp
