@@ -244,11 +244,10 @@ def run_absp(args, w, rank, world, local):
         with torch.cuda.graph(g, stream=stream):
             da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
         graphs.append(g)
-        blocks_ptr, stride, counts_ptr = da.last_selection(l)
+        _, stride, _ = da.last_selection(l)
         ga = torch.cuda.CUDAGraph()
         with torch.cuda.graph(ga, stream=stream):
-            da._lib.absp_attend(da._ctx, l, layers[l]["q"].data_ptr(), blocks_ptr, stride, counts_ptr,
-                                layers[l]["out"].data_ptr(), stream.cuda_stream)
+            da.attend_selected(l, layers[l]["q"], layers[l]["out"], stream)
         att_graphs.append(ga)
         sel_blocks = torch.empty(B, H, stride, dtype=torch.int32, device=dev)
         sel_counts = torch.empty(B, H, dtype=torch.int32, device=dev)
@@ -338,7 +337,7 @@ def run_absp(args, w, rank, world, local):
                        "l2": f"{L} rotating layers x {step_bytes / 1e6:.0f} MB algorithmic bytes per step (> 126 MB L2)",
                        "parallelism": f"batch-sharded x{world}, no collective",
                        "compute": "int4 codes -> exact fp32 scores; bf16 MMA (mma.sync) fp32 accumulate"},
-            "roofline": {"bound": "hbm", "kernel": "absp_attend (k_attn + k_merge)",
+            "roofline": {"bound": "hbm", "kernel": "k_attn (absp_attend_selected: paged flash-decode + fused LSE merge)",
                          "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                          "traffic": None, "bytes_per_launch": attn_bytes, "peak_source": peak_src},
             "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms_step / 1e3) / 1e9,

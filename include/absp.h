@@ -153,6 +153,12 @@ absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* 
 absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint32_t* blocks,
                         uint32_t blocks_stride, const uint32_t* counts, float* out, void* stream);
 
+/* sparse_attention over the layer's most recent selection (made by absp_select or
+ * absp_decode_step): the attention half of a decode step, e.g. to run it on another
+ * stream than the selection. */
+absp_status absp_attend_selected(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
+                                 void* stream);
+
 /* select + attend using context-owned selection buffers (the per-step hot path). */
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
                              void* stream);

@@ -268,6 +268,10 @@ class DecodeAttention:
         check(self._lib.absp_attend(self._ctx, layer, _ptr(q), _ptr(blocks), stride, _ptr(counts),
                                     _ptr(out), _stream(stream)))
 
+    def attend_selected(self, layer: int, q, out, stream=None) -> None:
+        """Attention over the layer's most recent selection (second half of decode_step)."""
+        check(self._lib.absp_attend_selected(self._ctx, layer, _ptr(q), _ptr(out), _stream(stream)))
+
     def decode_step(self, layer: int, q, out, stream=None) -> None:
         check(self._lib.absp_decode_step(self._ctx, layer, _ptr(q), _ptr(out), _stream(stream)))
 

@@ -62,20 +62,30 @@ struct LayerView {
 cudaError_t launch_build_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches);
 cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreItem* items,
                          uint32_t n_items, cudaStream_t s, int* launches);
+// Selected blocks resolved to pool pages, per unit: slot s = entry * (B/P) + page.
+struct PageList {
+    uint32_t* page;   // [units][stride] pool page id
+    uint16_t* valid;  // [units][stride] valid rows of the page (0 = empty slot)
+    uint32_t stride;  // slots per unit
+};
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
-                        uint32_t* blocks, uint32_t stride, uint32_t* counts, cudaStream_t s,
-                        int* launches);
+                        uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
+                        cudaStream_t s, int* launches);
+cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
+                                 const uint32_t* counts, const PageList& pages, cudaStream_t s,
+                                 int* launches);
 // Attention work list: all 128-row chunks of all units, unit-major.
 struct AttendWork {
     const uint32_t* chunk_unit;  // [n_work] unit of each chunk
+    const uint32_t* chunk_idx;   // [n_work] chunk index within its unit
     const uint32_t* chunk_base;  // [units + 1] first chunk of each unit
     uint32_t n_work;             // total chunks
     uint32_t slots_per_unit;     // partial slots reserved per unit (max chunks of a unit)
     uint32_t* unit_done;         // [units] completion counters (zero between launches)
     uint32_t grid;               // persistent CTAs (one per SM)
 };
-cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const uint32_t* blocks,
-                          uint32_t stride, const uint32_t* counts, const AttendWork& work,
+cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages,
+                          const uint32_t* counts, const AttendWork& work,
                           float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches);
 size_t attend_smem_bytes(uint32_t D, uint32_t P);

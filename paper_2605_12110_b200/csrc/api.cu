@@ -74,17 +74,23 @@ struct DevBuf {
 
 // Device-side attention work list (see AttendWork).
 struct WorkList {
-    DevBuf<uint32_t> chunk_unit, chunk_base, unit_done;
-    uint32_t n_work = 0, slots = 0;
+    DevBuf<uint32_t> chunk_unit, chunk_idx, chunk_base, unit_done;
+    DevBuf<uint32_t> page;    // resolved page list, [units][page_stride]
+    DevBuf<uint16_t> valid;
+    uint32_t n_work = 0, slots = 0, page_stride = 0;
     void release() {
         chunk_unit.release();
+        chunk_idx.release();
         chunk_base.release();
         unit_done.release();
+        page.release();
+        valid.release();
     }
+    PageList pages() const { return PageList{page.p, valid.p, page_stride}; }
 };
 
 struct Layer {
-    bool assigned = false, bound = false, built = false;
+    bool assigned = false, bound = false, built = false, selected = false;
     std::vector<uint32_t> block_sizes;
     const uint16_t* k_pool = nullptr;
     const uint16_t* v_pool = nullptr;
@@ -106,7 +112,7 @@ struct Layer {
     DevBuf<float> values, values_min, scales, zps, scales_min, zps_min, scores;
     DevBuf<uint32_t> codes, codes_min;
     DevBuf<uint32_t> sel_blocks, sel_counts;
-    DevBuf<float> part_o, part_ml;
+    DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
     DevBuf<float> stage_out;
 
@@ -186,8 +192,8 @@ uint32_t chunks_for(uint32_t entries, uint32_t block) {
 
 // Builds the chunk list for units holding at most min(N, cap) entries (cap = K for
 // decode, blocks_stride for explicit selections) and sizes the partial buffers.
-absp_status build_work(Layer& l, uint32_t D, bool decode, uint32_t cap, WorkList& wl) {
-    std::vector<uint32_t> base(l.desc.size() + 1, 0), unit_of;
+absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t cap, WorkList& wl) {
+    std::vector<uint32_t> base(l.desc.size() + 1, 0), unit_of, idx_of;
     uint32_t slots = 1;
     for (size_t u = 0; u < l.desc.size(); ++u) {
         const UnitDesc& d = l.desc[u];
@@ -196,15 +202,22 @@ absp_status build_work(Layer& l, uint32_t D, bool decode, uint32_t cap, WorkList
         base[u + 1] = base[u] + ch;
         slots = std::max(slots, ch);
         unit_of.insert(unit_of.end(), ch, uint32_t(u));
+        for (uint32_t c = 0; c < ch; ++c) idx_of.push_back(c);
     }
     wl.n_work = base.back();
     wl.slots = slots;
+    wl.page_stride = slots * (kAttnChunkRows / P);  // page slots per unit
     ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
+    ABSP_CUDA(wl.chunk_idx.ensure(idx_of.size()));
     ABSP_CUDA(wl.chunk_base.ensure(base.size()));
     ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
+    ABSP_CUDA(wl.page.ensure(l.desc.size() * size_t(wl.page_stride)));
+    ABSP_CUDA(wl.valid.ensure(l.desc.size() * size_t(wl.page_stride)));
     ABSP_CUDA(cudaMemcpy(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4, cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
+    ABSP_CUDA(cudaMemset(wl.valid.p, 0, l.desc.size() * size_t(wl.page_stride) * 2));
     ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(slots) * 8 * D));
     ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(slots) * 16));
     return ABSP_OK;
@@ -213,6 +226,7 @@ absp_status build_work(Layer& l, uint32_t D, bool decode, uint32_t cap, WorkList
 AttendWork work_view(const WorkList& wl, int num_sms) {
     AttendWork w{};
     w.chunk_unit = wl.chunk_unit.p;
+    w.chunk_idx = wl.chunk_idx.p;
     w.chunk_base = wl.chunk_base.p;
     w.n_work = wl.n_work;
     w.slots_per_unit = wl.slots;
@@ -353,6 +367,9 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     if (batch == 0 || batch > c.max_batch)
         return fail(ABSP_EINVAL, "kv_bind: batch must be in 1..max_batch");
     if (pool_pages == 0) return fail(ABSP_EINVAL, "kv_bind: pool_pages must be positive");
+    if (pool_pages * c.num_kv_heads > 0xffffffffull)
+        return fail(ABSP_EINVAL, "kv_bind: num_kv_heads * pool_pages must fit in 32 bits");
+    l->selected = false;
     uint32_t max_len = 0;
     for (uint32_t b = 0; b < batch; ++b) {
         if (seq_lens[b] == 0)
@@ -430,11 +447,7 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     ABSP_CUDA(l->sel_counts.ensure(units));
     for (auto& kv : l->attend_work) kv.second.release();
     l->attend_work.clear();
-    st = build_work(*l, c.head_dim, true, 0, l->step_work);
-    if (st != ABSP_OK) return st;
-    // the explicit-selection work list for the context's own stride is prebuilt so
-    // that absp_attend on decode selections can be graph-captured
-    st = build_work(*l, c.head_dim, false, l->sel_stride, l->attend_work[l->sel_stride]);
+    st = build_work(*l, c.head_dim, c.page_size, true, 0, l->step_work);
     if (st != ABSP_OK) return st;
     ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
@@ -458,15 +471,28 @@ absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream) {
     return ABSP_OK;
 }
 
+// Scoring + top-k; the top-k kernel also resolves the selection into the decode
+// work list's page list, consumed by the attention producer.
 static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* blocks,
                              uint32_t stride, uint32_t* counts, cudaStream_t s) {
     const LayerView v = view_of(ctx, *l);
     int n = 0;
     cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), l->d_items.p,
                                  uint32_t(l->items.size()), s, &n);
-    if (e == cudaSuccess) e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, s, &n);
+    if (e == cudaSuccess)
+        e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "select kernels");
+    return ABSP_OK;
+}
+
+static absp_status do_attend_step(absp_ctx* ctx, Layer* l, const void* q, float* out, cudaStream_t s) {
+    int n = 0;
+    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->step_work.pages(),
+                                  l->sel_counts.p, work_view(l->step_work, ctx->num_sms), l->part_o.p,
+                                  l->part_ml.p, out, s, &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
 }
 
@@ -481,7 +507,9 @@ absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* 
         return fail(ABSP_EINVAL, "select: blocks_stride " + std::to_string(blocks_stride) +
                                      " < max_select " + std::to_string(l->max_select));
     DeviceGuard dg(ctx->device);
-    return do_select(ctx, l, q, blocks, blocks_stride, counts, cudaStream_t(stream));
+    st = do_select(ctx, l, q, blocks, blocks_stride, counts, cudaStream_t(stream));
+    if (st == ABSP_OK) l->selected = true;
+    return st;
 }
 
 absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint32_t* blocks,
@@ -493,21 +521,36 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     if (!q || !blocks || !counts || !out) return fail(ABSP_EINVAL, "attend: null pointer");
     if (blocks_stride == 0) return fail(ABSP_EINVAL, "attend: blocks_stride must be positive");
     DeviceGuard dg(ctx->device);
-    // Work list for selections of up to min(N, blocks_stride) entries per unit;
-    // built once per stride (the first call for a new stride allocates).
+    // Work list + page list for selections of up to min(N, blocks_stride) entries
+    // per unit; built once per stride (the first call for a new stride allocates).
     auto it = l->attend_work.find(blocks_stride);
     if (it == l->attend_work.end()) {
-        st = build_work(*l, ctx->cfg.head_dim, false, blocks_stride, l->attend_work[blocks_stride]);
+        st = build_work(*l, ctx->cfg.head_dim, ctx->cfg.page_size, false, blocks_stride,
+                        l->attend_work[blocks_stride]);
         if (st != ABSP_OK) return st;
         it = l->attend_work.find(blocks_stride);
     }
+    const LayerView v = view_of(ctx, *l);
+    const cudaStream_t s = cudaStream_t(stream);
     int n = 0;
-    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), blocks,
-                                  blocks_stride, counts, work_view(it->second, ctx->num_sms),
-                                  l->part_o.p, l->part_ml.p, out, cudaStream_t(stream), &n);
+    cudaError_t e = launch_resolve_pages(v, blocks, blocks_stride, counts, it->second.pages(), s, &n);
+    if (e == cudaSuccess)
+        e = launch_attend(v, static_cast<const uint16_t*>(q), it->second.pages(), counts,
+                          work_view(it->second, ctx->num_sms), l->part_o.p, l->part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
+}
+
+absp_status absp_attend_selected(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
+                                 void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->selected) return fail(ABSP_ESTATE, "attend_selected: no selection made on this layer");
+    if (!q || !out) return fail(ABSP_EINVAL, "attend_selected: null pointer");
+    DeviceGuard dg(ctx->device);
+    return do_attend_step(ctx, l, q, out, cudaStream_t(stream));
 }
 
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
@@ -521,13 +564,8 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     const cudaStream_t s = cudaStream_t(stream);
     st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, s);
     if (st != ABSP_OK) return st;
-    int n = 0;
-    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->sel_blocks.p,
-                                  l->sel_stride, l->sel_counts.p, work_view(l->step_work, ctx->num_sms),
-                                  l->part_o.p, l->part_ml.p, out, s, &n);
-    ctx->launches += n;
-    if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
-    return ABSP_OK;
+    l->selected = true;
+    return do_attend_step(ctx, l, q, out, s);
 }
 
 absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_host,

@@ -132,10 +132,9 @@ __device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
-                                                      const uint32_t* __restrict__ blocks,
-                                                      uint32_t stride,
-                                                      const uint32_t* __restrict__ counts,
+                                                      PageList pages,
                                                       const uint32_t* __restrict__ chunk_unit,
+                                                      const uint32_t* __restrict__ chunk_idx,
                                                       const uint32_t* __restrict__ chunk_base,
                                                       uint32_t n_work, uint32_t slots_per_unit,
                                                       float* __restrict__ part_o,
@@ -166,37 +165,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 
     if (warp == kConsumers / 32) {
         // ============================ producer ================================
+        // The page list (resolved by the top-k kernel) of chunk w+1 is fetched while
+        // chunk w waits for a free stage, so the two dependent L2 round trips
+        // (chunk -> unit, unit -> pages) stay off the copy-issue path. Lane k*32+l
+        // owns page slot k*32+l (NS <= 128 slots -> up to 4 per lane).
+        constexpr int SPL = kMaxSlots / 32;
+        uint32_t nu = 0, ncx = 0, ngp[SPL], nvl[SPL];
+        auto fetch = [&](uint32_t w) {
+            if (w >= w_end) return;
+            nu = __ldg(chunk_unit + w);
+            ncx = __ldg(chunk_idx + w);
+            const size_t base = size_t(nu) * pages.stride + size_t(ncx) * NS;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const uint32_t s = k * 32 + lane;
+                ngp[k] = s < NS ? __ldcg(pages.page + base + s) : 0u;
+                nvl[k] = s < NS ? __ldcg(pages.valid + base + s) : 0u;
+            }
+        };
+        fetch(w_begin);
         uint32_t stage = 0, phase = 0;
         for (uint32_t w = w_begin; w < w_end; ++w) {
+            const uint32_t u = nu, c = ncx;
+            uint32_t gp[SPL], vl[SPL];
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                gp[k] = ngp[k];
+                vl[k] = nvl[k];
+            }
+            fetch(w + 1);
             mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
-            const uint32_t u = chunk_unit[w];
-            const uint32_t c = w - chunk_base[u];
-            const UnitDesc du = L.desc[u];
-            const uint32_t B = du.block;
-            const uint32_t E = kRows / B;
-            const uint32_t ppb = B / P;  // pages per block
-            const uint32_t cnt = counts[u];
-            const uint32_t j0 = c * E;
-            const uint32_t ne = j0 < cnt ? min(E, cnt - j0) : 0u;
             StageMeta& mt = sh.meta[stage];
             const uint32_t kdst = smem_base + stage * 2 * TB;
             const uint32_t full = smem_u32(&sh.full[stage]);
-            const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
-            // pass 1: lane = page slot; which slots hold tokens, how many bytes
             uint32_t bytes = 0, invalid = 0;
-            for (uint32_t s0 = 0; s0 < NS; s0 += 32) {
-                const uint32_t s = s0 + lane;
-                uint32_t valid = 0;
-                if (s < NS) {
-                    const uint32_t e = s / ppb, pp = s % ppb;
-                    if (e < ne) {
-                        const uint32_t t0 = __ldg(blocks + size_t(u) * stride + j0 + e) * B + pp * P;
-                        if (t0 < du.n_tokens) valid = min(P, du.n_tokens - t0);
-                    }
-                    mt.valid[s] = uint16_t(valid);
-                }
-                bytes += __reduce_add_sync(0xffffffffu, valid ? 2 * P * D * 2 : 0u);
-                invalid |= __ballot_sync(0xffffffffu, s < NS && valid < P);
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const uint32_t s = k * 32 + lane;
+                if (s < NS) mt.valid[s] = uint16_t(vl[k]);
+                bytes += __reduce_add_sync(0xffffffffu, vl[k] ? 2 * P * D * 2 : 0u);
+                invalid |= __ballot_sync(0xffffffffu, s < NS && vl[k] < P);
             }
             if (lane == 0) {
                 mt.unit = u;
@@ -205,15 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 mbar_expect_tx(full, bytes);
             }
             __syncwarp();
-            // pass 2: issue the copies (slot lookups re-read from L1)
-            for (uint32_t s0 = 0; s0 < NS; s0 += 32) {
-                const uint32_t s = s0 + lane;
-                if (s < NS && mt.valid[s]) {
-                    const uint32_t e = s / ppb, pp = s % ppb;
-                    const uint32_t blk = __ldg(blocks + size_t(u) * stride + j0 + e);
-                    const uint32_t t0 = blk * B + pp * P;
-                    const uint32_t page = __ldg(pt + t0 / P);
-                    const size_t off = (size_t(du.head) * L.pool_pages + page) * P * D;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const uint32_t s = k * 32 + lane;
+                if (s < NS && vl[k]) {
+                    const size_t off = size_t(gp[k]) * P * D;  // gp = head * pool_pages + page
                     bulk_g2s(kdst + s * slot_stride, L.k_pool + off, P * D * 2, full);
                     bulk_g2s(kdst + TB + s * slot_stride, L.v_pool + off, P * D * 2, full);
                 }
@@ -473,19 +477,19 @@ cudaError_t init_attend_attributes() {
                                 int(attend_smem_bytes(128, 1)));
 }
 
-cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const uint32_t* blocks,
-                          uint32_t stride, const uint32_t* counts, const AttendWork& wk,
-                          float* part_o, float* part_ml, float* out, cudaStream_t s,
-                          int* launches) {
+cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages,
+                          const uint32_t* counts, const AttendWork& wk, float* part_o,
+                          float* part_ml, float* out, cudaStream_t s, int* launches) {
+    (void)counts;  // chunk page lists carry the selection (empty slots have valid = 0)
     const size_t smem = attend_smem_bytes(L.D, L.P);
     const uint32_t grid = wk.n_work < wk.grid ? wk.n_work : wk.grid;
     if (grid == 0) return cudaSuccess;
     if (L.D == 64)
-        k_attn<64><<<grid, kThreads, smem, s>>>(L, q, blocks, stride, counts, wk.chunk_unit, wk.chunk_base,
+        k_attn<64><<<grid, kThreads, smem, s>>>(L, q, pages, wk.chunk_unit, wk.chunk_idx, wk.chunk_base,
                                                 wk.n_work, wk.slots_per_unit, part_o, part_ml, wk.unit_done,
                                                 out);
     else
-        k_attn<128><<<grid, kThreads, smem, s>>>(L, q, blocks, stride, counts, wk.chunk_unit, wk.chunk_base,
+        k_attn<128><<<grid, kThreads, smem, s>>>(L, q, pages, wk.chunk_unit, wk.chunk_idx, wk.chunk_base,
                                                  wk.n_work, wk.slots_per_unit, part_o, part_ml, wk.unit_done,
                                                  out);
     ++*launches;

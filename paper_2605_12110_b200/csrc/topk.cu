@@ -9,18 +9,21 @@
 //
 // Algorithm (one 512-thread CTA per unit, no atomics on the hot loop):
 //   1. Order-preserving u32 keys (+-0 folded to +0), loaded once into registers
-//      (ITEMS keys per thread, warp-step s = j*16 + warp covers indices
-//      [32s, 32s+32)). Units with more than 512*64 blocks use the same code with
-//      keys re-read from L2 each pass.
-//   2. The bits shared by every key (AND vs OR reduction) are skipped; the
-//      remaining bits are resolved MSB-first by an exact radix select with 5-bit
-//      digits: 32 bins == 32 lanes. Per warp-step, 5 ballots give each lane (=bin)
-//      its count through a LOP chain + POPC — ~10 warp instructions per 32 keys,
-//      no shared-memory atomics. This pins the (K-1)-th largest key tau and how
-//      many tau-valued keys are still needed; ties at tau go to the lowest indices.
-//   3. The <= K winners are gathered to shared memory as 64-bit composite keys
-//      (key << 32 | ~index), all distinct, and bitonic-sorted descending, which
-//      is exactly the reference order.
+//      (ITEMS keys per thread; warp-step s = j*16 + warp covers [32s, 32s+32)).
+//      Units with more than 512*64 blocks re-read the keys from L2 each pass.
+//   2. Bits shared by every key (AND vs OR reduction) are skipped; the rest are
+//      resolved MSB-first by an exact radix select with 5-bit digits: 32 bins ==
+//      32 lanes; per warp-step, 5 ballots give each lane (= bin) its count through
+//      a LOP chain + POPC. As soon as the keys still matching the running prefix
+//      fit in shared memory they are compacted there, and the remaining passes
+//      touch only them. This pins the (K-1)-th largest key tau and how many
+//      tau-valued keys are still needed; ties at tau go to the lowest indices.
+//   3. The <= K winners become 64-bit composite keys (key << 32 | ~index), all
+//      distinct; their rank among each other is their output position (rank sort
+//      for K <= 256, bitonic sort above), which is exactly the reference order.
+//   4. The kernel also resolves every selected block to its pool pages (the
+//      reference's populate_page_spans, engine.cpp:271-283) for the attention
+//      producer: page id and valid-row count per page slot.
 #include "absp_internal.cuh"
 
 namespace absp {
@@ -29,7 +32,8 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSort = 2048;   // max K
-constexpr int kMaxSteps = 4096;  // max (N-1)/32 warp-steps for tie ranking
+constexpr int kMaxSteps = 4096;  // max (N-1)/32 warp-steps for index tie ranking
+constexpr int kCompact = 2048;   // compaction capacity (keys matching the prefix)
 
 __device__ __forceinline__ uint32_t order_key(float f) {
     uint32_t u = __float_as_uint(f);
@@ -40,13 +44,18 @@ __device__ __forceinline__ uint32_t order_key(float f) {
 struct TopkSmem {
     uint32_t hist[kWarps][32];
     uint32_t red[2][kWarps];
-    uint32_t state[4];  // prefix, pmask, remaining, eq_total
+    uint32_t state[6];  // prefix, pmask, remaining, eq_total, compacted count, compact flag
     uint32_t nsel;
     unsigned long long sel[kMaxSort];
-    uint32_t eq[kMaxSteps];
+    union {
+        uint32_t eq[kMaxSteps];
+        struct {
+            uint32_t key[kCompact];
+            uint32_t idx[kCompact];
+        } c;
+    } u;
 };
 
-// Key of warp-step item j: from registers (REG) or re-read from L2.
 template <bool REG, int ITEMS>
 struct Keys {
     uint32_t r[REG ? ITEMS : 1];
@@ -58,9 +67,21 @@ struct Keys {
     }
 };
 
+// One radix pass over a warp-step's 32 keys: adds this lane's bin count.
+__device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t prefix, uint32_t pmask,
+                                              int shift, int nbits, const uint32_t* xm) {
+    const uint32_t m = __ballot_sync(0xffffffffu, in && (key & pmask) == prefix);
+    if (m == 0u) return 0u;
+    uint32_t mm = m;
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+        if (b < nbits) mm &= __ballot_sync(0xffffffffu, (key >> (shift + b)) & 1u) ^ xm[b];
+    return __popc(mm);
+}
+
 template <bool REG, int ITEMS>
 __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
-                                                   uint32_t* counts) {
+                                                   uint32_t* counts, PageList pages) {
     __shared__ TopkSmem sm;
     const uint32_t u = blockIdx.x;
     const UnitDesc du = L.desc[u];
@@ -70,7 +91,6 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t sel_total = N <= K ? N : K;
     const uint32_t n_cand = N > K ? N - 1 : 0u;  // radix-select domain [0, N-1)
-    // number of warp-steps each warp walks
     const uint32_t nsteps = (n_cand + 31) / 32;
     const int my_items = REG ? ITEMS : int((nsteps + kWarps - 1 - warp) / kWarps);
 
@@ -89,8 +109,13 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
         sm.state[1] = 0u;
         sm.state[2] = N > K ? K - 1 : 0u;
         sm.state[3] = 0u;
+        sm.state[4] = 0u;
+        sm.state[5] = 0u;
         sm.nsel = 0u;
     }
+    uint32_t xm[5];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) xm[b] = ((lane >> b) & 1u) ? 0u : 0xffffffffu;
 
     if (N > K && K > 1) {
         // ---- common prefix of all candidate keys ---------------------------
@@ -119,8 +144,8 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
             kor |= sm.red[1][w];
         }
         const uint32_t diff = kand ^ kor;
-        int lo_bit;  // bits [lo_bit, 32) are already decided
-        if (diff == 0u) {  // every candidate key is equal
+        int lo_bit;  // bits [lo_bit, 32) are decided
+        if (diff == 0u) {
             if (threadIdx.x == 0) {
                 sm.state[0] = kand;
                 sm.state[1] = 0xffffffffu;
@@ -128,36 +153,58 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
             }
             lo_bit = 0;
         } else {
-            lo_bit = 32 - __clz(diff);  // highest differing bit is lo_bit-1
+            lo_bit = 32 - __clz(diff);
             if (threadIdx.x == 0) {
                 const uint32_t m = lo_bit >= 32 ? 0u : (0xffffffffu << lo_bit);
                 sm.state[0] = kand & m;
                 sm.state[1] = m;
+                sm.state[3] = n_cand;
             }
         }
         __syncthreads();
 
         // ---- radix select, 5-bit digits, MSB first ------------------------
-        uint32_t xm[5];
-#pragma unroll
-        for (int b = 0; b < 5; ++b) xm[b] = ((lane >> b) & 1u) ? 0u : 0xffffffffu;
+        bool compact = false;
         while (lo_bit > 0) {
+            const uint32_t prefix = sm.state[0], pmask = sm.state[1];
+            // compact the keys still matching the prefix once they fit
+            if (!compact && sm.state[3] <= uint32_t(kCompact)) {
+#pragma unroll
+                for (int j = 0; j < my_items; ++j) {
+                    const uint32_t i = (j * kWarps + warp) * 32 + lane;
+                    const uint32_t key = keys.get(j, i);
+                    const bool in = i < n_cand && (key & pmask) == prefix;
+                    const uint32_t m = __ballot_sync(0xffffffffu, in);
+                    if (m) {
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(&sm.state[4], __popc(m));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (in) {
+                            const uint32_t p = base + __popc(m & ((1u << lane) - 1u));
+                            sm.u.c.key[p] = key;
+                            sm.u.c.idx[p] = i;
+                        }
+                    }
+                }
+                compact = true;
+                __syncthreads();
+            }
             const int nbits = lo_bit >= 5 ? 5 : lo_bit;
             const int shift = lo_bit - nbits;
-            const uint32_t prefix = sm.state[0], pmask = sm.state[1];
             uint32_t cnt = 0;
-#pragma unroll
-            for (int j = 0; j < my_items; ++j) {
-                const uint32_t i = (j * kWarps + warp) * 32 + lane;
-                const uint32_t key = keys.get(j, i);
-                const uint32_t m = __ballot_sync(0xffffffffu, i < n_cand && (key & pmask) == prefix);
-                if (m == 0u) continue;
-                uint32_t mm = m;
-#pragma unroll
-                for (int b = 0; b < 5; ++b) {
-                    if (b < nbits) mm &= __ballot_sync(0xffffffffu, (key >> (shift + b)) & 1u) ^ xm[b];
+            if (compact) {
+                const uint32_t nc = sm.state[4];
+                for (uint32_t s = warp; s * 32 < nc; s += kWarps) {
+                    const uint32_t i = s * 32 + lane;
+                    const uint32_t key = i < nc ? sm.u.c.key[i] : 0u;
+                    cnt += bin_count(i < nc, key, prefix, pmask, shift, nbits, xm);
                 }
-                cnt += __popc(mm);
+            } else {
+#pragma unroll
+                for (int j = 0; j < my_items; ++j) {
+                    const uint32_t i = (j * kWarps + warp) * 32 + lane;
+                    cnt += bin_count(i < n_cand, keys.get(j, i), prefix, pmask, shift, nbits, xm);
+                }
             }
             if (lane >= (1u << nbits)) cnt = 0;
             sm.hist[warp][lane] = cnt;
@@ -184,6 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
             __syncthreads();
             lo_bit = shift;
         }
+        if (threadIdx.x == 0) sm.state[5] = compact ? 1u : 0u;
     }
     __syncthreads();
 
@@ -196,46 +244,13 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
         const uint32_t need_eq = sm.state[2];
         const bool use_tau = K > 1;
         const bool all_eq = use_tau && need_eq == sm.state[3];
-        if (use_tau && !all_eq) {  // tie ranking by index among tau-valued keys
-#pragma unroll
-            for (int j = 0; j < my_items; ++j) {
-                const uint32_t s = j * kWarps + warp;
-                const uint32_t i = s * 32 + lane;
-                const uint32_t m = __ballot_sync(0xffffffffu, i < n_cand && keys.get(j, i) == tau);
-                if (lane == 0) sm.eq[s] = __popc(m);
-            }
-            __syncthreads();
-            if (warp == 0) {  // exclusive scan over warp-steps (index order)
-                uint32_t carry = 0;
-                for (uint32_t base = 0; base < nsteps; base += 32) {
-                    const uint32_t v = base + lane < nsteps ? sm.eq[base + lane] : 0u;
-                    uint32_t incl = v;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= uint32_t(o)) incl += t;
-                    }
-                    if (base + lane < nsteps) sm.eq[base + lane] = carry + incl - v;
-                    carry += __shfl_sync(0xffffffffu, incl, 31);
-                }
-            }
-            __syncthreads();
-        }
+        const bool compacted = sm.state[5] != 0;
+        // keys strictly above tau (and all tau-valued keys when every one is taken)
 #pragma unroll
         for (int j = 0; j < my_items; ++j) {
-            const uint32_t s = j * kWarps + warp;
-            const uint32_t i = s * 32 + lane;
+            const uint32_t i = (j * kWarps + warp) * 32 + lane;
             const uint32_t key = keys.get(j, i);
-            bool take = false;
-            if (use_tau) {
-                if (all_eq) {
-                    take = i < n_cand && key >= tau;
-                } else {
-                    const uint32_t eqm = __ballot_sync(0xffffffffu, i < n_cand && key == tau);
-                    const uint32_t rank = sm.eq[s] + __popc(eqm & ((1u << lane) - 1u));
-                    take = i < n_cand && (key > tau || (key == tau && rank < need_eq));
-                }
-            }
+            const bool take = use_tau && i < n_cand && (key > tau || (all_eq && key == tau));
             const uint32_t tm = __ballot_sync(0xffffffffu, take);
             if (tm) {
                 uint32_t base = 0;
@@ -244,55 +259,186 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
                 if (take) sm.sel[base + __popc(tm & ((1u << lane) - 1u))] = (uint64_t(key) << 32) | uint32_t(~i);
             }
         }
+        if (use_tau && !all_eq) {
+            // only `need_eq` of the tau-valued keys fit: the lowest indices win
+            if (compacted) {
+                const uint32_t nc = sm.state[4];
+                for (uint32_t p = threadIdx.x; p < nc; p += kThreads) {
+                    if (sm.u.c.key[p] != tau) continue;
+                    const uint32_t my = sm.u.c.idx[p];
+                    uint32_t rank = 0;
+                    for (uint32_t o = 0; o < nc; ++o) rank += (sm.u.c.key[o] == tau && sm.u.c.idx[o] < my);
+                    if (rank < need_eq) {
+                        const uint32_t pos = atomicAdd(&sm.nsel, 1u);
+                        sm.sel[pos] = (uint64_t(tau) << 32) | uint32_t(~my);
+                    }
+                }
+            } else {
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < my_items; ++j) {
+                    const uint32_t s = j * kWarps + warp;
+                    const uint32_t i = s * 32 + lane;
+                    const uint32_t m = __ballot_sync(0xffffffffu, i < n_cand && keys.get(j, i) == tau);
+                    if (lane == 0) sm.u.eq[s] = __popc(m);
+                }
+                __syncthreads();
+                if (warp == 0) {  // exclusive scan over warp-steps (index order)
+                    uint32_t carry = 0;
+                    for (uint32_t base = 0; base < nsteps; base += 32) {
+                        const uint32_t v = base + lane < nsteps ? sm.u.eq[base + lane] : 0u;
+                        uint32_t incl = v;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= uint32_t(o)) incl += t;
+                        }
+                        if (base + lane < nsteps) sm.u.eq[base + lane] = carry + incl - v;
+                        carry += __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < my_items; ++j) {
+                    const uint32_t s = j * kWarps + warp;
+                    const uint32_t i = s * 32 + lane;
+                    const bool eq = i < n_cand && keys.get(j, i) == tau;
+                    const uint32_t eqm = __ballot_sync(0xffffffffu, eq);
+                    const bool take = eq && sm.u.eq[s] + __popc(eqm & ((1u << lane) - 1u)) < need_eq;
+                    const uint32_t tm = __ballot_sync(0xffffffffu, take);
+                    if (tm) {
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(&sm.nsel, __popc(tm));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (take) sm.sel[base + __popc(tm & ((1u << lane) - 1u))] = (uint64_t(tau) << 32) | uint32_t(~i);
+                    }
+                }
+            }
+        }
         if (threadIdx.x == 0) {
             const uint32_t t = N - 1;
             sm.sel[K - 1] = (uint64_t(order_key(sc[t])) << 32) | uint32_t(~t);
         }
     }
-    uint32_t sp = 1;
-    while (sp < sel_total) sp <<= 1;
-    for (uint32_t i = sel_total + threadIdx.x; i < sp; i += kThreads) sm.sel[i] = 0ull;
     __syncthreads();
 
-    // ---- bitonic sort, descending ------------------------------------------
-    for (uint32_t k = 2; k <= sp; k <<= 1) {
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < sp; i += kThreads) {
-                const uint32_t ixj = i ^ j;
-                if (ixj > i) {
-                    const unsigned long long a = sm.sel[i], b = sm.sel[ixj];
-                    const bool desc = (i & k) == 0;
-                    if (desc ? (a < b) : (a > b)) {
-                        sm.sel[i] = b;
-                        sm.sel[ixj] = a;
+    // ---- order: (key desc, index asc) == composite desc -----------------------
+    uint32_t* out = blocks + size_t(u) * stride;
+    if (sel_total <= 256) {
+        // rank sort: position = number of larger composites (all distinct)
+        for (uint32_t i = threadIdx.x; i < sel_total; i += kThreads) {
+            const unsigned long long me = sm.sel[i];
+            uint32_t rank = 0;
+            for (uint32_t o = 0; o < sel_total; ++o) rank += sm.sel[o] > me;
+            out[rank] = ~uint32_t(me);
+        }
+    } else {
+        uint32_t sp = 1;
+        while (sp < sel_total) sp <<= 1;
+        for (uint32_t i = sel_total + threadIdx.x; i < sp; i += kThreads) sm.sel[i] = 0ull;
+        __syncthreads();
+        for (uint32_t k = 2; k <= sp; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < sp; i += kThreads) {
+                    const uint32_t ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long a = sm.sel[i], b = sm.sel[ixj];
+                        const bool desc = (i & k) == 0;
+                        if (desc ? (a < b) : (a > b)) {
+                            sm.sel[i] = b;
+                            sm.sel[ixj] = a;
+                        }
                     }
                 }
+                __syncthreads();
             }
-            __syncthreads();
+        }
+        for (uint32_t i = threadIdx.x; i < sel_total; i += kThreads) out[i] = ~uint32_t(sm.sel[i]);
+    }
+    if (threadIdx.x == 0) counts[u] = sel_total;
+
+    // ---- resolve selected blocks to pool pages (populate_page_spans) ----------
+    if (pages.page) {
+        // slot s = entry * (B/P) + page; slots up to the end of the last 128-row
+        // attention chunk of the unit are written (empty ones with valid = 0)
+        const uint32_t ppb = du.block / L.P;
+        const uint32_t E = kAttnChunkRows / du.block;
+        const uint32_t slot_end = ((sel_total + E - 1) / E) * E * ppb;
+        const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+        const uint32_t head_base = du.head * uint32_t(L.pool_pages);
+        uint32_t* pg = pages.page + size_t(u) * pages.stride;
+        uint16_t* vl = pages.valid + size_t(u) * pages.stride;
+        __syncthreads();  // `out` written by the sort above is visible block-wide
+        for (uint32_t s = threadIdx.x; s < slot_end; s += kThreads) {
+            const uint32_t e = s / ppb, pp = s % ppb;
+            uint32_t v = 0, page = 0;
+            if (e < sel_total) {
+                const uint32_t t0 = out[e] * du.block + pp * L.P;
+                if (t0 < du.n_tokens) {
+                    v = min(L.P, du.n_tokens - t0);
+                    page = head_base + __ldg(pt + t0 / L.P);
+                }
+            }
+            pg[s] = page;
+            vl[s] = uint16_t(v);
         }
     }
-    uint32_t* out = blocks + size_t(u) * stride;
-    for (uint32_t i = threadIdx.x; i < sel_total; i += kThreads) out[i] = ~uint32_t(sm.sel[i]);
-    if (threadIdx.x == 0) counts[u] = sel_total;
 }
 
 }  // namespace
 
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
-                        uint32_t* blocks, uint32_t stride, uint32_t* counts, cudaStream_t s,
-                        int* launches) {
+                        uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
+                        cudaStream_t s, int* launches) {
     if (max_budget > uint32_t(kMaxSort) || max_nblocks > uint32_t(kMaxSteps) * 32u)
         return cudaErrorInvalidValue;
     const uint32_t per_thread = (max_nblocks + kThreads - 1) / kThreads;
     const dim3 grid(L.units);
-    if (per_thread <= 1) k_topk<true, 1><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else if (per_thread <= 2) k_topk<true, 2><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else if (per_thread <= 4) k_topk<true, 4><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else if (per_thread <= 8) k_topk<true, 8><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else if (per_thread <= 16) k_topk<true, 16><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else if (per_thread <= 32) k_topk<true, 32><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else if (per_thread <= 64) k_topk<true, 64><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
-    else k_topk<false, 1><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts);
+#define ABSP_TOPK(REG, IT) k_topk<REG, IT><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts, pages)
+    if (per_thread <= 1) ABSP_TOPK(true, 1);
+    else if (per_thread <= 2) ABSP_TOPK(true, 2);
+    else if (per_thread <= 4) ABSP_TOPK(true, 4);
+    else if (per_thread <= 8) ABSP_TOPK(true, 8);
+    else if (per_thread <= 16) ABSP_TOPK(true, 16);
+    else if (per_thread <= 32) ABSP_TOPK(true, 32);
+    else if (per_thread <= 64) ABSP_TOPK(true, 64);
+    else ABSP_TOPK(false, 1);
+#undef ABSP_TOPK
+    ++*launches;
+    return cudaGetLastError();
+}
+
+// Page resolution for an explicit (caller-provided) selection: absp_attend.
+__global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks, uint32_t stride,
+                                const uint32_t* __restrict__ counts, PageList pages) {
+    const uint32_t u = blockIdx.x;
+    const UnitDesc du = L.desc[u];
+    const uint32_t ppb = du.block / L.P;
+    const uint32_t E = kAttnChunkRows / du.block;
+    const uint32_t cap = min(stride, du.n_blocks);  // entries the work list reserves
+    const uint32_t cnt = min(counts[u], cap);
+    const uint32_t slot_end = ((cap + E - 1) / E) * E * ppb;
+    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+    const uint32_t head_base = du.head * uint32_t(L.pool_pages);
+    for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
+        const uint32_t e = s / ppb, pp = s % ppb;
+        uint32_t v = 0, page = 0;
+        if (e < cnt) {
+            const uint32_t t0 = __ldg(blocks + size_t(u) * stride + e) * du.block + pp * L.P;
+            if (t0 < du.n_tokens) {
+                v = min(L.P, du.n_tokens - t0);
+                page = head_base + __ldg(pt + t0 / L.P);
+            }
+        }
+        pages.page[size_t(u) * pages.stride + s] = page;
+        pages.valid[size_t(u) * pages.stride + s] = uint16_t(v);
+    }
+}
+
+cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
+                                 const uint32_t* counts, const PageList& pages, cudaStream_t s,
+                                 int* launches) {
+    k_resolve_pages<<<L.units, 256, 0, s>>>(L, blocks, stride, counts, pages);
     ++*launches;
     return cudaGetLastError();
 }
