@@ -13,12 +13,13 @@
 // form one list; a persistent grid (one CTA per SM) takes contiguous ranges of it,
 // so every SM streams the same number of KV bytes regardless of block sizes.
 //
-// CTA = 4 consumer warps + 1 producer warp, 3-stage mbarrier ring:
+// CTA = 2 groups of 4 consumer warps + 1 producer warp, 3-stage mbarrier ring:
 //   producer : lane s resolves page slot s of the next chunk (selected block ->
 //              page table -> pool page) and issues one cp.async.bulk per page for K
 //              and V (the TMA bulk-copy engine; 1 instruction per 1-4 KB page),
 //              completing on the stage's full barrier.
-//   consumers: S^T = K Q^T and O^T += V^T P^T on mma.m16n8k16 (M = 16 KV rows or
+//   consumers: (two groups take alternate chunks so their latency chains overlap)
+//              S^T = K Q^T and O^T += V^T P^T on mma.m16n8k16 (M = 16 KV rows or
 //              channels, N = 8 query heads of the GQA group), fp32 online softmax
 //              across the chunks of a unit, P kept as a bf16 hi/lo pair (~16
 //              mantissa bits). A run of chunks of one unit ends in a partial
@@ -39,8 +40,10 @@ namespace absp {
 namespace {
 
 constexpr int kRows = kAttnChunkRows;  // 128
-constexpr int kConsumers = 128;        // 4 warps
-constexpr int kThreads = kConsumers + 32;
+constexpr int kGroupThreads = 128;     // one consumer group = 4 warps
+constexpr int kGroups = 2;             // consumer groups working on alternate chunks
+constexpr int kConsumers = kGroupThreads * kGroups;
+constexpr int kThreads = kConsumers + 32;  // + 1 producer warp
 constexpr int kStages = 3;
 constexpr int kPStride = kRows + 8;    // bf16 row stride of P (bank-conflict free)
 constexpr int kMaxSlots = kRows;       // P >= 1
@@ -74,8 +77,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory");
+__device__ __forceinline__ void group_sync(uint32_t grp) {  // named barrier 1 + grp
+    asm volatile("bar.sync %0, %1;\n" ::"r"(grp + 1), "n"(kGroupThreads) : "memory");
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
@@ -112,13 +115,17 @@ struct StageMeta {
     uint16_t valid[kMaxSlots];  // valid rows per page slot (0..P)
 };
 
+struct GroupSmem {
+    uint16_t p[2][8 * kPStride];  // P as bf16 hi + bf16 residual
+    float red[2][4][8];           // per-warp max / sum per head
+    uint32_t flag;
+};
+
 struct SmemHead {  // fixed-size part after the stage tiles
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     StageMeta meta[kStages];
-    uint16_t p[2][8 * kPStride];  // P as bf16 hi + bf16 residual
-    float red[2][4][8];
-    uint32_t flag;
+    GroupSmem grp[kGroups];
 };
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&sh.full[s]), 1);
-            mbar_init(smem_u32(&sh.empty[s]), kConsumers / 32);
+            mbar_init(smem_u32(&sh.empty[s]), kGroupThreads / 32);  // one consumer group
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -231,37 +238,59 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     }
 
     // ============================== consumers =================================
+    // Two groups of 4 warps take alternate chunks (local chunk i -> group i % 2), so
+    // one group's MMA/softmax latency chain overlaps the other's. Each group keeps its
+    // own online-softmax state and emits its own partials.
+    const uint32_t grp = warp / 4, wg = warp % 4, gtid = tid % kGroupThreads;
+    GroupSmem& gs = sh.grp[grp];
     const uint32_t g = lane >> 2, t4 = lane & 3;
     const uint32_t G = L.G;
     const float scale_log2 = rsqrtf(float(D)) * 1.4426950408889634f;
-    uint32_t stage = 0, phase = 0;
+    const uint32_t ns_log = 31 - __clz(NS);  // NS = 128 / P is a power of two
+    // logical row i of a chunk -> byte offset inside a tile
+    auto row_off = [&](uint32_t i) -> uint32_t {
+        return (i & (NS - 1)) * slot_stride + (i >> ns_log) * (D * 2);
+    };
+    // per-thread smem offsets, identical for every chunk
+    uint32_t qk_off[2], pv_off[kRows / 16], rv_slot[2][2], rv_row[2][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        qk_off[m] = row_off(wg * 32 + m * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) + (lane >> 4) * 16;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t row = wg * 32 + m * 16 + g + hh * 8;
+            rv_slot[m][hh] = row & (NS - 1);
+            rv_row[m][hh] = row >> ns_log;
+        }
+    }
+#pragma unroll
+    for (int ks = 0; ks < kRows / 16; ++ks)
+        pv_off[ks] = row_off(ks * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) + ((lane >> 3) & 1) * 16;
+
     uint32_t cur_u = 0xffffffffu, seg_first = 0, seg_last = 0;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // logical row i of a chunk -> byte offset inside a tile
-    auto row_off = [&](uint32_t i) -> uint32_t { return (i % NS) * slot_stride + (i / NS) * (D * 2); };
-
-    // Emit the partial of (cur_u, chunks seg_first..seg_last); the CTA completing the
-    // unit merges all of its partials into `out`.
+    // Emit this group's partial of (cur_u, its chunks seg_first, seg_first+2, .., seg_last);
+    // the contributor completing the unit merges all of the unit's partials into `out`.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
-        consumer_sync();  // red[] free
+        group_sync(grp);  // red[] free
         if (g == 0) {
-            sh.red[1][warp][2 * t4] = lsum[0];
-            sh.red[1][warp][2 * t4 + 1] = lsum[1];
+            gs.red[1][wg][2 * t4] = lsum[0];
+            gs.red[1][wg][2 * t4 + 1] = lsum[1];
         }
         const size_t slot = size_t(cur_u) * slots_per_unit + seg_first;
         float* po = part_o + slot * 8 * D;
         float* ml = part_ml + slot * 16;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-            const uint32_t c0 = warp * (D / 4) + mt * 16 + g;
+            const uint32_t c0 = wg * (D / 4) + mt * 16 + g;
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
                 const uint32_t h = 2 * t4 + hc;
@@ -271,35 +300,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 }
             }
         }
-        if (warp == 0 && g == 0) {  // m is block-uniform per head
+        if (wg == 0 && g == 0) {  // m is group-uniform per head
             ml[(2 * t4) * 2] = m_run[0];
             ml[(2 * t4 + 1) * 2] = m_run[1];
         }
-        consumer_sync();
-        if (tid < 8)
-            ml[tid * 2 + 1] = sh.red[1][0][tid] + sh.red[1][1][tid] + sh.red[1][2][tid] + sh.red[1][3][tid];
-        // chunks of this run after the first carry no partial of their own
-        for (uint32_t c = seg_first + 1 + tid / 8; c <= seg_last; c += kConsumers / 8) {
+        group_sync(grp);
+        if (gtid < 8)
+            ml[gtid * 2 + 1] = gs.red[1][0][gtid] + gs.red[1][1][gtid] + gs.red[1][2][gtid] + gs.red[1][3][gtid];
+        // this group's other chunks of the run carry no partial of their own
+        for (uint32_t c = seg_first + kGroups * (1 + gtid / 8); c <= seg_last; c += kGroups * (kGroupThreads / 8)) {
             float* mc = part_ml + (size_t(cur_u) * slots_per_unit + c) * 16;
-            mc[(tid % 8) * 2] = -INFINITY;
-            mc[(tid % 8) * 2 + 1] = 0.0f;
+            mc[(gtid % 8) * 2] = -INFINITY;
+            mc[(gtid % 8) * 2 + 1] = 0.0f;
         }
         // ---- completion counting; the last contributor merges ------------------
         __threadfence();
-        consumer_sync();
+        group_sync(grp);
         const uint32_t total = chunk_base[cur_u + 1] - chunk_base[cur_u];
-        if (tid == 0) {
-            const uint32_t mine = seg_last - seg_first + 1;
+        if (gtid == 0) {
+            const uint32_t mine = (seg_last - seg_first) / kGroups + 1;
             const uint32_t done = atomicAdd(unit_done + cur_u, mine) + mine;
-            sh.flag = done == total ? 1u : 0u;
+            gs.flag = done == total ? 1u : 0u;
             if (done == total) unit_done[cur_u] = 0u;  // re-arm for the next step
         }
-        consumer_sync();
-        if (sh.flag) {
+        group_sync(grp);
+        if (gs.flag) {
             __threadfence();
             const UnitDesc du = L.desc[cur_u];
             const float* mlu = part_ml + size_t(cur_u) * slots_per_unit * 16;
-            for (uint32_t h = warp; h < G; h += kConsumers / 32) {
+            for (uint32_t h = wg; h < G; h += kGroupThreads / 32) {
                 float M = -INFINITY;
                 for (uint32_t c = lane; c < total; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
 #pragma unroll
@@ -326,7 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     };
 
-    for (uint32_t w = w_begin; w < w_end; ++w) {
+    for (uint32_t i = grp; w_begin + i < w_end; i += kGroups) {
+        const uint32_t stage = i % kStages, phase = (i / kStages) & 1u;
         mbar_wait(smem_u32(&sh.full[stage]), phase);
         const StageMeta& mt = sh.meta[stage];
         const uint32_t u = mt.unit;
@@ -353,26 +383,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         if (any_invalid) {
             // zero the V rows that carry no token: stale or uninitialised smem could
             // hold NaN/Inf, and 0 * NaN would poison the PV product
-            for (uint32_t i = tid; i < kRows * (D / 8); i += kConsumers) {
-                const uint32_t row = i / (D / 8), ch = i % (D / 8);
-                if ((row / NS) >= mt.valid[row % NS]) {
+            for (uint32_t e = gtid; e < kRows * (D / 8); e += kGroupThreads) {
+                const uint32_t row = e / (D / 8), ch = e % (D / 8);
+                if ((row >> ns_log) >= mt.valid[row & (NS - 1)]) {
                     unsigned char* p = smem + stage * 2 * TB + TB + row_off(row) + ch * 16;
                     *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
                 }
             }
+            group_sync(grp);
         }
 
-        // S^T = K Q^T: warp w owns logical rows [32w, 32w+32)
+        // S^T = K Q^T: warp wg owns logical rows [32wg, 32wg+32)
         float s[2][4];
 #pragma unroll
-        for (int m = 0; m < 2; ++m) {
-            s[m][0] = s[m][1] = s[m][2] = s[m][3] = 0.0f;
-            const uint32_t row = warp * 32 + m * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-            const uint32_t ra = k_base + row_off(row);
+        for (int m = 0; m < 2; ++m) s[m][0] = s[m][1] = s[m][2] = s[m][3] = 0.0f;
 #pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
+        for (int ks = 0; ks < D / 16; ++ks) {
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
                 uint32_t a0, a1, a2, a3;
-                ldsm_x4(ra + (ks * 2 + (lane >> 4)) * 16, a0, a1, a2, a3);
+                ldsm_x4(k_base + qk_off[m] + ks * 32, a0, a1, a2, a3);
                 mma_bf16(s[m], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
             }
         }
@@ -380,10 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
         for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const uint32_t row = warp * 32 + m * 16 + g + hh * 8;
-                rv[m][hh] = !any_invalid || (row / NS) < mt.valid[row % NS];
-            }
+            for (int hh = 0; hh < 2; ++hh) rv[m][hh] = !any_invalid || rv_row[m][hh] < mt.valid[rv_slot[m][hh]];
         float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
         for (int m = 0; m < 2; ++m)
@@ -397,15 +424,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) mx[hc] = fmaxf(mx[hc], __shfl_xor_sync(0xffffffffu, mx[hc], off));
         if (g == 0) {
-            sh.red[0][warp][2 * t4] = mx[0];
-            sh.red[0][warp][2 * t4 + 1] = mx[1];
+            gs.red[0][wg][2 * t4] = mx[0];
+            gs.red[0][wg][2 * t4 + 1] = mx[1];
         }
-        consumer_sync();
+        group_sync(grp);
         float mnew[2];
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc) {
             const int h = 2 * t4 + hc;
-            const float cm = fmaxf(fmaxf(sh.red[0][0][h], sh.red[0][1][h]), fmaxf(sh.red[0][2][h], sh.red[0][3][h]));
+            const float cm = fmaxf(fmaxf(gs.red[0][0][h], gs.red[0][1][h]), fmaxf(gs.red[0][2][h], gs.red[0][3][h]));
             mnew[hc] = fmaxf(m_run[hc], cm * scale_log2);
             const float alpha = mnew[hc] == -INFINITY ? 1.0f : exp2f(m_run[hc] - mnew[hc]);
             m_run[hc] = mnew[hc];
@@ -418,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
-            const uint32_t r0 = warp * 32 + m * 16 + g;
+            const uint32_t r0 = wg * 32 + m * 16 + g;
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
                 const float p0 = rv[m][0] ? exp2f(fmaf(s[m][hc], scale_log2, -mnew[hc])) : 0.0f;
@@ -426,38 +453,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 l_run[hc] += p0 + p1;
                 const int h = 2 * t4 + hc;
                 const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
-                sh.p[0][h * kPStride + r0] = h0;
-                sh.p[0][h * kPStride + r0 + 8] = h1;
-                sh.p[1][h * kPStride + r0] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
-                sh.p[1][h * kPStride + r0 + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
+                gs.p[0][h * kPStride + r0] = h0;
+                gs.p[0][h * kPStride + r0 + 8] = h1;
+                gs.p[1][h * kPStride + r0] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
+                gs.p[1][h * kPStride + r0 + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
             }
         }
-        consumer_sync();
+        group_sync(grp);
 
-        // O^T += V^T P^T: warp w owns channels [w*D/4, (w+1)*D/4)
+        // O^T += V^T P^T: warp wg owns channels [wg*D/4, (wg+1)*D/4)
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-            const uint32_t cbase = warp * (D / 4) + m * 16;
+        for (int ks = 0; ks < kRows / 16; ++ks) {
+            const uint16_t* pp0 = gs.p[0] + g * kPStride + ks * 16 + 2 * t4;
+            const uint16_t* pp1 = gs.p[1] + g * kPStride + ks * 16 + 2 * t4;
+            const uint32_t b00 = *reinterpret_cast<const uint32_t*>(pp0);
+            const uint32_t b01 = *reinterpret_cast<const uint32_t*>(pp0 + 8);
+            const uint32_t b10 = *reinterpret_cast<const uint32_t*>(pp1);
+            const uint32_t b11 = *reinterpret_cast<const uint32_t*>(pp1 + 8);
 #pragma unroll
-            for (int ks = 0; ks < kRows / 16; ++ks) {
-                const uint32_t row = ks * 16 + (lane & 7) + ((lane >> 4) & 1) * 8;
-                const uint32_t ch = cbase / 8 + ((lane >> 3) & 1);
+            for (int m = 0; m < MT; ++m) {
                 uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(v_base + row_off(row) + ch * 16, a0, a1, a2, a3);
-#pragma unroll
-                for (int part = 0; part < 2; ++part) {
-                    const uint16_t* pp = sh.p[part] + g * kPStride + ks * 16 + 2 * t4;
-                    mma_bf16(o[m], a0, a1, a2, a3, *reinterpret_cast<const uint32_t*>(pp),
-                             *reinterpret_cast<const uint32_t*>(pp + 8));
-                }
+                ldsm_x4_t(v_base + pv_off[ks] + (wg * (D / 4) + m * 16) * 2, a0, a1, a2, a3);
+                mma_bf16(o[m], a0, a1, a2, a3, b00, b01);
+                mma_bf16(o[m], a0, a1, a2, a3, b10, b11);
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
-        if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-        }
     }
     if (cur_u != 0xffffffffu) flush();
 }

@@ -79,8 +79,41 @@ __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t pr
     return __popc(mm);
 }
 
+// Resolve the ordered selection `out` of unit u to pool pages for the attention
+// producer (the reference's populate_page_spans, engine.cpp:271-283): slot
+// s = entry * (B/P) + page; slots up to the end of the unit's last 128-row
+// attention chunk are written, empty ones with valid = 0. Block sizes and P are
+// powers of two (checked by absp_config_validate), so no divisions.
+__device__ __forceinline__ void resolve_pages(const LayerView& L, const UnitDesc& du, uint32_t u,
+                                              uint32_t sel_total, const uint32_t* out,
+                                              const PageList& pages) {
+    if (!pages.page) return;
+    const uint32_t ppb_log = __ffs(du.block) - __ffs(L.P);  // log2(B / P)
+    const uint32_t p_log = __ffs(L.P) - 1;
+    const uint32_t E = kAttnChunkRows / du.block;
+    const uint32_t slot_end = ((sel_total + E - 1) / E * E) << ppb_log;
+    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+    const uint32_t head_base = du.head * uint32_t(L.pool_pages);
+    uint32_t* pg = pages.page + size_t(u) * pages.stride;
+    uint16_t* vl = pages.valid + size_t(u) * pages.stride;
+    __syncthreads();  // `out` (global) written by this block is visible block-wide
+    for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
+        const uint32_t e = s >> ppb_log, pp = s & ((1u << ppb_log) - 1u);
+        uint32_t v = 0, page = 0;
+        if (e < sel_total) {
+            const uint32_t t0 = out[e] * du.block + (pp << p_log);
+            if (t0 < du.n_tokens) {
+                v = min(L.P, du.n_tokens - t0);
+                page = head_base + __ldg(pt + (t0 >> p_log));
+            }
+        }
+        pg[s] = page;
+        vl[s] = uint16_t(v);
+    }
+}
+
 template <bool REG, int ITEMS>
-__global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
+__global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
                                                    uint32_t* counts, PageList pages) {
     __shared__ TopkSmem sm;
     const uint32_t u = blockIdx.x;
@@ -116,6 +149,164 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
     uint32_t xm[5];
 #pragma unroll
     for (int b = 0; b < 5; ++b) xm[b] = ((lane >> b) & 1u) ? 0u : 0xffffffffu;
+    __syncthreads();
+
+    // ======== fast path: threshold from group maxima, exact order among few ========
+    // x = lower edge of the (15-bit) bucket holding the (K-1)-th largest maximum of
+    // groups of 4 keys. At least K-1 groups have a maximum >= x, so the candidates
+    // {key >= x} contain the whole top-(K-1); typically only a little more than K-1
+    // of them exist. They are compacted and ordered exactly among themselves.
+    if (REG && N > K && K > 1) {
+        constexpr int GS = ITEMS >= 4 ? 4 : 1;
+        constexpr int NG = ITEMS / GS;
+        const uint32_t K1 = K - 1;
+        uint32_t gmax[NG];
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+            uint32_t mx = 0;
+#pragma unroll
+            for (int j = gi * GS; j < gi * GS + GS; ++j) mx = max(mx, keys.r[j]);  // invalid keys are 0
+            gmax[gi] = mx;
+        }
+        uint32_t kand = 0xffffffffu, kor = 0u;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi)
+            if (((gi * GS) * kWarps + warp) * 32 + lane < n_cand) {
+                kand &= gmax[gi];
+                kor |= gmax[gi];
+            }
+        kand = __reduce_and_sync(0xffffffffu, kand);
+        kor = __reduce_or_sync(0xffffffffu, kor);
+        if (lane == 0) {
+            sm.red[0][warp] = kand;
+            sm.red[1][warp] = kor;
+        }
+        __syncthreads();
+        kand = 0xffffffffu;
+        kor = 0u;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            kand &= sm.red[0][w];
+            kor |= sm.red[1][w];
+        }
+        int lo_bit = (kand ^ kor) ? 32 - __clz(kand ^ kor) : 0;
+        uint32_t prefix = lo_bit >= 32 ? 0u : (kand & (0xffffffffu << lo_bit));
+        uint32_t pmask = lo_bit >= 32 ? 0u : (0xffffffffu << lo_bit);
+        uint32_t rem = K1;
+        for (int pass = 0; pass < 3 && lo_bit > 0; ++pass) {
+            const int nbits = lo_bit >= 5 ? 5 : lo_bit;
+            const int shift = lo_bit - nbits;
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                const bool in = ((gi * GS) * kWarps + warp) * 32 + lane < n_cand;
+                cnt += bin_count(in, gmax[gi], prefix, pmask, shift, nbits, xm);
+            }
+            if (lane >= (1u << nbits)) cnt = 0;
+            sm.hist[warp][lane] = cnt;
+            __syncthreads();
+            if (warp == 0) {
+                uint32_t tot = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) tot += sm.hist[w][lane];
+                uint32_t incl = tot;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_down_sync(0xffffffffu, incl, o);
+                    if (lane + o < 32) incl += v;
+                }
+                const uint32_t above = incl - tot;
+                if (tot > 0 && above < rem && rem <= above + tot) {
+                    sm.state[0] = prefix | (lane << shift);
+                    sm.state[2] = rem - above;
+                }
+            }
+            __syncthreads();
+            prefix = sm.state[0];
+            rem = sm.state[2];
+            pmask |= ((1u << nbits) - 1u) << shift;
+            lo_bit = shift;
+        }
+        const uint32_t x = prefix;  // bucket lower edge: low bits zero
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) c += keys.r[j] >= x && (j * kWarps + warp) * 32 + lane < n_cand;
+        c = __reduce_add_sync(0xffffffffu, c);
+        __syncthreads();
+        if (lane == 0) sm.red[0][warp] = c;
+        __syncthreads();
+        uint32_t C = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) C += sm.red[0][w];
+        if (C >= K1 && C <= uint32_t(kMaxSort)) {
+            // compact the candidates as composite keys (key << 32 | ~index)
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t i = (j * kWarps + warp) * 32 + lane;
+                const bool in = i < n_cand && keys.r[j] >= x;
+                const uint32_t m = __ballot_sync(0xffffffffu, in);
+                if (m) {
+                    uint32_t base = 0;
+                    if (lane == 0) base = atomicAdd(&sm.state[4], __popc(m));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (in) sm.sel[base + __popc(m & ((1u << lane) - 1u))] = (uint64_t(keys.r[j]) << 32) | uint32_t(~i);
+                }
+            }
+            __syncthreads();
+            const unsigned long long ct = (uint64_t(order_key(sc[N - 1])) << 32) | uint32_t(~(N - 1));
+            uint32_t* out = blocks + size_t(u) * stride;
+            if (C <= 256) {
+                // rank among candidates = output position (composites are distinct)
+                for (uint32_t p = threadIdx.x; p < C; p += kThreads) {
+                    const unsigned long long me = sm.sel[p];
+                    uint32_t rank = 0;
+                    for (uint32_t o = 0; o < C; ++o) rank += sm.sel[o] > me;
+                    if (rank < K1) {
+                        out[rank + (ct > me ? 1u : 0u)] = ~uint32_t(me);
+                        if (me > ct) atomicAdd(&sm.nsel, 1u);
+                    }
+                }
+            } else {
+                uint32_t sp = 1;
+                while (sp < C) sp <<= 1;
+                for (uint32_t i = C + threadIdx.x; i < sp; i += kThreads) sm.sel[i] = 0ull;
+                __syncthreads();
+                for (uint32_t k = 2; k <= sp; k <<= 1)
+                    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                        for (uint32_t i = threadIdx.x; i < sp; i += kThreads) {
+                            const uint32_t ixj = i ^ j;
+                            if (ixj > i) {
+                                const unsigned long long a = sm.sel[i], b = sm.sel[ixj];
+                                if (((i & k) == 0) ? (a < b) : (a > b)) {
+                                    sm.sel[i] = b;
+                                    sm.sel[ixj] = a;
+                                }
+                            }
+                        }
+                        __syncthreads();
+                    }
+                for (uint32_t p = threadIdx.x; p < K1; p += kThreads) {
+                    const unsigned long long me = sm.sel[p];
+                    out[p + (ct > me ? 1u : 0u)] = ~uint32_t(me);
+                    if (me > ct) atomicAdd(&sm.nsel, 1u);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                out[sm.nsel] = N - 1;  // the trailing block sits after every larger winner
+                counts[u] = K;
+            }
+            resolve_pages(L, du, u, K, out, pages);
+            return;
+        }
+        // too many candidates (heavy ties near the threshold): exact path below
+        if (threadIdx.x == 0) {
+            sm.state[0] = 0u;
+            sm.state[2] = K - 1;
+            sm.state[4] = 0u;
+        }
+        __syncthreads();
+    }
 
     if (N > K && K > 1) {
         // ---- common prefix of all candidate keys ---------------------------
@@ -356,33 +547,7 @@ __global__ void __launch_bounds__(kThreads) k_topk(LayerView L, uint32_t* blocks
         for (uint32_t i = threadIdx.x; i < sel_total; i += kThreads) out[i] = ~uint32_t(sm.sel[i]);
     }
     if (threadIdx.x == 0) counts[u] = sel_total;
-
-    // ---- resolve selected blocks to pool pages (populate_page_spans) ----------
-    if (pages.page) {
-        // slot s = entry * (B/P) + page; slots up to the end of the last 128-row
-        // attention chunk of the unit are written (empty ones with valid = 0)
-        const uint32_t ppb = du.block / L.P;
-        const uint32_t E = kAttnChunkRows / du.block;
-        const uint32_t slot_end = ((sel_total + E - 1) / E) * E * ppb;
-        const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
-        const uint32_t head_base = du.head * uint32_t(L.pool_pages);
-        uint32_t* pg = pages.page + size_t(u) * pages.stride;
-        uint16_t* vl = pages.valid + size_t(u) * pages.stride;
-        __syncthreads();  // `out` written by the sort above is visible block-wide
-        for (uint32_t s = threadIdx.x; s < slot_end; s += kThreads) {
-            const uint32_t e = s / ppb, pp = s % ppb;
-            uint32_t v = 0, page = 0;
-            if (e < sel_total) {
-                const uint32_t t0 = out[e] * du.block + pp * L.P;
-                if (t0 < du.n_tokens) {
-                    v = min(L.P, du.n_tokens - t0);
-                    page = head_base + __ldg(pt + t0 / L.P);
-                }
-            }
-            pg[s] = page;
-            vl[s] = uint16_t(v);
-        }
-    }
+    resolve_pages(L, du, u, sel_total, out, pages);
 }
 
 }  // namespace
