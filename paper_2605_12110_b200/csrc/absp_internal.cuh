@@ -96,6 +96,6 @@ cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint
 // Rows per attention chunk (one CTA), see attend.cu.
 constexpr uint32_t kAttnChunkRows = 128;
 // Centroids per scoring CTA, see score.cu.
-constexpr uint32_t kScoreItemCentroids = 512;
+constexpr uint32_t kScoreItemCentroids = 2048;
 
 }  // namespace absp

@@ -21,7 +21,8 @@ namespace absp {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPerThread = kScoreItemCentroids / kThreads;  // centroids per thread
+constexpr int kPerThread = kScoreItemCentroids / kThreads;  // centroids per thread per item
+constexpr int kBatch = 2;                                    // centroids per thread per batch
 
 __device__ __forceinline__ float bf16f(uint16_t x) { return __uint_as_float(uint32_t(x) << 16); }
 
@@ -39,76 +40,118 @@ __device__ __forceinline__ void load_query(const LayerView& L, const UnitDesc& d
     }
 }
 
-// Table path: bits in {2, 4}; MAXMIN doubles the tables and code streams.
+// Byte offset (code * 4) of nibble/crumb k of a packed code word, for a 4-byte
+// table entry. 4-bit: two masked copies hold the even / odd nibbles pre-scaled by 4
+// in their bytes, and one PRMT per code extracts a byte (1.5 ALU ops per code).
+template <int BITS>
+struct CodeOffsets {
+    uint32_t a, b, w;
+    __device__ __forceinline__ explicit CodeOffsets(uint32_t word) : w(word) {
+        if (BITS == 4) {
+            a = (word << 2) & 0x3c3c3c3cu;  // nibbles 0,2,4,6 (x4) in bytes 0..3
+            b = (word >> 2) & 0x3c3c3c3cu;  // nibbles 1,3,5,7 (x4)
+        }
+    }
+    __device__ __forceinline__ uint32_t operator()(int k) const {
+        if (BITS == 4) return __byte_perm((k & 1) ? b : a, 0u, 0x4440u | uint32_t(k >> 1));
+        return ((w >> (k * BITS)) & ((1u << BITS) - 1u)) << 2;
+    }
+};
+
+// Table path: bits in {2, 4}; MAXMIN doubles the tables and code streams. A CTA
+// scores one item (up to kScoreItemCentroids centroids of one unit) in batches of
+// kThreads * kBatch, with the next batch's code words loaded while the current
+// batch is scored.
 template <int D, int BITS, bool ASYM, bool MAXMIN>
-__global__ void __launch_bounds__(kThreads) k_score_tbl(LayerView L, const uint16_t* q,
-                                                        const ScoreItem* items) {
+__global__ void __launch_bounds__(kThreads, 2) k_score_tbl(LayerView L, const uint16_t* q,
+                                                           const ScoreItem* items) {
     constexpr int LV = 1 << BITS;
     constexpr int W = D * BITS / 32;
     constexpr int CPW = 32 / BITS;
-    constexpr uint32_t MASK = LV - 1;
+    constexpr int NT = MAXMIN ? 2 : 1;
+    constexpr int NW = MAXMIN ? 2 * W : W;  // words per centroid incl. the min array
     __shared__ float qs[D];
-    __shared__ float tbl[(MAXMIN ? 2 : 1) * D * LV];
+    __shared__ float prm[NT][2][D];
+    __shared__ __align__(16) float tbl[NT * D * LV];
 
     const ScoreItem it = items[blockIdx.x];
     const UnitDesc du = L.desc[it.unit];
+    const uint32_t end = min(it.start + uint32_t(kScoreItemCentroids), du.n_blocks);
     const uint32_t* codes = L.codes + du.seg * W;
     const uint32_t* codes_lo = MAXMIN ? L.codes_min + du.seg * W : nullptr;
     float* out = L.scores + du.seg;
 
-    // Issue every code-word load of this thread first (coalesced: one 128 B line per
-    // warp per word), so HBM latency overlaps the table construction below.
-    uint32_t idx[kPerThread];
-    bool ok[kPerThread];
+    auto load = [&](uint32_t base, uint32_t (&wd)[kBatch][NW]) {
 #pragma unroll
-    for (int j = 0; j < kPerThread; ++j) {
-        const uint32_t i = it.start + j * kThreads + threadIdx.x;
-        ok[j] = i < du.n_blocks;
-        idx[j] = ok[j] ? i : 0;
-    }
-    uint32_t word[kPerThread][W], wlo[kPerThread][MAXMIN ? W : 1];
+        for (int j = 0; j < kBatch; ++j) {
+            uint32_t i = base + j * kThreads + threadIdx.x;
+            i = i < end ? i : it.start;  // clamp: a valid centroid, result discarded
 #pragma unroll
-    for (int w = 0; w < W; ++w)
-#pragma unroll
-        for (int j = 0; j < kPerThread; ++j) {
-            word[j][w] = __ldg(codes + size_t(w) * du.cap + idx[j]);
-            if (MAXMIN) wlo[j][w] = __ldg(codes_lo + size_t(w) * du.cap + idx[j]);
-        }
-
-    load_query<D>(L, du, q, qs);
-    __syncthreads();
-    const int mid = (1 << (BITS - 1)) - 1;
-    for (int t = 0; t < (MAXMIN ? 2 : 1); ++t) {
-        const float* sc = (t ? L.scales_min : L.scales) + size_t(it.unit) * D;
-        const float* zp = (t ? L.zps_min : L.zps) + size_t(it.unit) * D;
-        for (uint32_t e = threadIdx.x; e < D * LV; e += kThreads) {
-            const uint32_t c = e / LV, k = e % LV;
-            const float deq = ASYM ? __fadd_rn(zp[c], __fmul_rn(float(k), sc[c]))
-                                   : __fmul_rn(float(int(k) - mid), sc[c]);
-            tbl[t * D * LV + e] = __fmul_rn(qs[c], deq);
-        }
-    }
-    __syncthreads();
-
-    float acc[kPerThread];
-#pragma unroll
-    for (int j = 0; j < kPerThread; ++j) acc[j] = 0.0f;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-#pragma unroll
-        for (int k = 0; k < CPW; ++k) {
-            const float* row = tbl + (w * CPW + k) * LV;
-#pragma unroll
-            for (int j = 0; j < kPerThread; ++j) {
-                float p = row[(word[j][w] >> (k * BITS)) & MASK];
-                if (MAXMIN) p = ref_max(p, row[D * LV + ((wlo[j][w] >> (k * BITS)) & MASK)]);
-                acc[j] = __fadd_rn(acc[j], p);
+            for (int w = 0; w < W; ++w) {
+                wd[j][w] = __ldg(codes + size_t(w) * du.cap + i);
+                if (MAXMIN) wd[j][W + w] = __ldg(codes_lo + size_t(w) * du.cap + i);
             }
         }
-    }
+    };
+    auto score = [&](uint32_t base, const uint32_t (&wd)[kBatch][NW]) {
+        float acc[kBatch];
 #pragma unroll
-    for (int j = 0; j < kPerThread; ++j)
-        if (ok[j]) out[idx[j]] = acc[j];
+        for (int j = 0; j < kBatch; ++j) acc[j] = 0.0f;
+        const char* tb = reinterpret_cast<const char*>(tbl);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            CodeOffsets<BITS> hi0(wd[0][w]), hi1(wd[kBatch - 1][w]);
+            CodeOffsets<BITS> lo0(MAXMIN ? wd[0][W + w] : 0u), lo1(MAXMIN ? wd[kBatch - 1][W + w] : 0u);
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) {
+                const char* row = tb + (w * CPW + k) * LV * 4;
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const CodeOffsets<BITS>& h = j == 0 ? hi0 : hi1;
+                    float p = *reinterpret_cast<const float*>(row + h(k));
+                    if (MAXMIN) {
+                        const CodeOffsets<BITS>& l = j == 0 ? lo0 : lo1;
+                        p = ref_max(p, *reinterpret_cast<const float*>(row + D * LV * 4 + l(k)));
+                    }
+                    acc[j] = __fadd_rn(acc[j], p);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const uint32_t i = base + j * kThreads + threadIdx.x;
+            if (i < end) out[i] = acc[j];
+        }
+    };
+
+    // batch 0's code words are in flight while the query, parameters and table are built
+    uint32_t wa[kBatch][NW], wb[kBatch][NW];
+    load(it.start, wa);
+
+    load_query<D>(L, du, q, qs);
+    for (uint32_t e = threadIdx.x; e < NT * 2 * D; e += kThreads) {
+        const uint32_t t = e / (2 * D), which = (e / D) & 1, c = e % D;
+        const float* src = which == 0 ? (t ? L.scales_min : L.scales) : (t ? L.zps_min : L.zps);
+        prm[t][which][c] = src[size_t(it.unit) * D + c];
+    }
+    __syncthreads();
+    const int mid = (1 << (BITS - 1)) - 1;
+    for (uint32_t e = threadIdx.x; e < NT * D * LV; e += kThreads) {
+        const uint32_t t = e / (D * LV), c = (e / LV) % D, k = e % LV;
+        const float sc = prm[t][0][c], zp = prm[t][1][c];
+        const float deq = ASYM ? __fadd_rn(zp, __fmul_rn(float(k), sc)) : __fmul_rn(float(int(k) - mid), sc);
+        tbl[e] = __fmul_rn(qs[c], deq);
+    }
+    __syncthreads();
+
+    constexpr uint32_t kStep = kThreads * kBatch;
+    for (uint32_t base = it.start; base < end; base += 2 * kStep) {
+        if (base + kStep < end) load(base + kStep, wb);
+        score(base, wa);
+        if (base + kStep >= end) break;
+        if (base + 2 * kStep < end) load(base + 2 * kStep, wa);
+        score(base + kStep, wb);
+    }
 }
 
 // Direct path for int8 codes (a 256-entry table per channel would not fit).
