@@ -191,6 +191,11 @@ def run_reference(args, w, rank, world):
 # ---------------------------------------------------------------------------
 # B200 path
 # ---------------------------------------------------------------------------
+def trace(msg):
+    if os.environ.get("ABSP_BENCH_TRACE"):
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_absp(args, w, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -227,6 +232,7 @@ def run_absp(args, w, rank, world, local):
             da.build_store(l, stream)
             layers.append(dict(k=k, v=v, q=q, out=out))
     stream.synchronize()
+    trace("layers built")
     info = da.layer_info(0)
     step_bytes, select_bytes, attn_kv_bytes = algorithmic_bytes(w, info.kv_bytes_selected, info.total_centroids, B)
     attn_bytes = attn_kv_bytes + B * H * G * d * (2 + 4)
@@ -239,6 +245,7 @@ def run_absp(args, w, rank, world, local):
             da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
     stream.synchronize()
     per_step_launches = (da.launch_count() - launches_before) // L
+    trace("eager warm-up done")
     for l in range(L):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
@@ -283,11 +290,15 @@ def run_absp(args, w, rank, world, local):
         return ms
 
     K, W = args.steps, max(args.warmup, 3)
+    trace("graphs captured")
     sampler = ClockSampler(local)
     with sampler:
         ms_step = timed(lambda i: graphs[i % L].replay(), K, W)
+    trace(f"step timed: {ms_step * 1e3:.1f} us")
     ms_attn = timed(lambda i: att_graphs[i % L].replay(), K, W)
+    trace(f"attend timed: {ms_attn * 1e3:.1f} us")
     ms_sel = timed(lambda i: sel_graphs[i % L][0].replay(), K, W)
+    trace(f"select timed: {ms_sel * 1e3:.1f} us")
 
     # end to end through the public C ABI with host buffers
     q_host = [torch.empty(B, H * G, d, dtype=torch.int16).pin_memory() for _ in range(L)]
@@ -307,6 +318,7 @@ def run_absp(args, w, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    trace(f"e2e timed: {e2e_s * 1e6:.1f} us")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res, err = cpu_reference(w, args.cpu_reps, 1)
