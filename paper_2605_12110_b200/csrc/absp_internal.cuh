@@ -93,8 +93,11 @@ cudaError_t init_attend_attributes();  // per device, once
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);
 
-// Rows per attention chunk (one CTA), see attend.cu.
+// Rows per attention chunk (one pipeline stage), see attend.cu.
 constexpr uint32_t kAttnChunkRows = 128;
+// Consumer groups per attention CTA; each owns a row split of every chunk and
+// emits its own partials (partial slots per chunk).
+constexpr uint32_t kAttnGroups = 2;
 // Centroids per scoring CTA, see score.cu.
 constexpr uint32_t kScoreItemCentroids = 2048;
 

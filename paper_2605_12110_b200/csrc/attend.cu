@@ -18,7 +18,7 @@
 //              page table -> pool page) and issues one cp.async.bulk per page for K
 //              and V (the TMA bulk-copy engine; 1 instruction per 1-4 KB page),
 //              completing on the stage's full barrier.
-//   consumers: (two groups take alternate chunks so their latency chains overlap)
+//   consumers: (two groups split each chunk's rows so their latency chains overlap)
 //              S^T = K Q^T and O^T += V^T P^T on mma.m16n8k16 (M = 16 KV rows or
 //              channels, N = 8 query heads of the GQA group), fp32 online softmax
 //              across the chunks of a unit, P kept as a bf16 hi/lo pair (~16
@@ -41,11 +41,12 @@ namespace {
 
 constexpr int kRows = kAttnChunkRows;  // 128
 constexpr int kGroupThreads = 128;     // one consumer group = 4 warps
-constexpr int kGroups = 2;             // consumer groups working on alternate chunks
+constexpr int kGroups = kAttnGroups;   // consumer groups, each owning half of every chunk
 constexpr int kConsumers = kGroupThreads * kGroups;
 constexpr int kThreads = kConsumers + 32;  // + 1 producer warp
 constexpr int kStages = 3;
-constexpr int kPStride = kRows + 8;    // bf16 row stride of P (bank-conflict free)
+constexpr int kGroupRows = kRows / 2;  // rows of a chunk owned by one consumer group
+constexpr int kPStride = kGroupRows + 8;  // bf16 row stride of P (bank-conflict free)
 constexpr int kMaxSlots = kRows;       // P >= 1
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&sh.full[s]), 1);
-            mbar_init(smem_u32(&sh.empty[s]), kGroupThreads / 32);  // one consumer group
+            mbar_init(smem_u32(&sh.empty[s]), kConsumers / 32);  // every consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -238,9 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     }
 
     // ============================== consumers =================================
-    // Two groups of 4 warps take alternate chunks (local chunk i -> group i % 2), so
-    // one group's MMA/softmax latency chain overlaps the other's. Each group keeps its
-    // own online-softmax state and emits its own partials.
+    // Both groups consume every stage; group g owns logical rows [64g, 64g+64) of
+    // each chunk (a row split with its own online-softmax state and partials), so
+    // the per-chunk MMA/softmax latency chain is half as long and the two groups'
+    // chains overlap. Every waiter sees every phase of every barrier in order.
     const uint32_t grp = warp / 4, wg = warp % 4, gtid = tid % kGroupThreads;
     GroupSmem& gs = sh.grp[grp];
     const uint32_t g = lane >> 2, t4 = lane & 3;
@@ -251,29 +253,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     auto row_off = [&](uint32_t i) -> uint32_t {
         return (i & (NS - 1)) * slot_stride + (i >> ns_log) * (D * 2);
     };
+    const uint32_t row0 = grp * kGroupRows;  // first logical row of this group
     // per-thread smem offsets, identical for every chunk
-    uint32_t qk_off[2], pv_off[kRows / 16], rv_slot[2][2], rv_row[2][2];
+    const uint32_t qk_off = row_off(row0 + wg * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) + (lane >> 4) * 16;
+    uint32_t rv_slot[2], rv_row[2], pv_off[kGroupRows / 16];
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-        qk_off[m] = row_off(wg * 32 + m * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) + (lane >> 4) * 16;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t row = wg * 32 + m * 16 + g + hh * 8;
-            rv_slot[m][hh] = row & (NS - 1);
-            rv_row[m][hh] = row >> ns_log;
-        }
+    for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t row = row0 + wg * 16 + g + hh * 8;
+        rv_slot[hh] = row & (NS - 1);
+        rv_row[hh] = row >> ns_log;
     }
 #pragma unroll
-    for (int ks = 0; ks < kRows / 16; ++ks)
-        pv_off[ks] = row_off(ks * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) + ((lane >> 3) & 1) * 16;
+    for (int ks = 0; ks < kGroupRows / 16; ++ks)
+        pv_off[ks] = row_off(row0 + ks * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) + ((lane >> 3) & 1) * 16;
 
     uint32_t cur_u = 0xffffffffu, seg_first = 0, seg_last = 0;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // Emit this group's partial of (cur_u, its chunks seg_first, seg_first+2, .., seg_last);
-    // the contributor completing the unit merges all of the unit's partials into `out`.
+    // partial slot of (unit, first chunk of a run, group)
+    auto slot_of = [&](uint32_t unit, uint32_t chunk, uint32_t gr) -> size_t {
+        return (size_t(unit) * slots_per_unit + chunk) * kGroups + gr;
+    };
+
+    // Emit this group's partial of (cur_u, chunks seg_first..seg_last); the
+    // contributor completing the unit merges all of the unit's partials into `out`.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             gs.red[1][wg][2 * t4] = lsum[0];
             gs.red[1][wg][2 * t4 + 1] = lsum[1];
         }
-        const size_t slot = size_t(cur_u) * slots_per_unit + seg_first;
+        const size_t slot = slot_of(cur_u, seg_first, grp);
         float* po = part_o + slot * 8 * D;
         float* ml = part_ml + slot * 16;
 #pragma unroll
@@ -307,30 +312,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         group_sync(grp);
         if (gtid < 8)
             ml[gtid * 2 + 1] = gs.red[1][0][gtid] + gs.red[1][1][gtid] + gs.red[1][2][gtid] + gs.red[1][3][gtid];
-        // this group's other chunks of the run carry no partial of their own
-        for (uint32_t c = seg_first + kGroups * (1 + gtid / 8); c <= seg_last; c += kGroups * (kGroupThreads / 8)) {
-            float* mc = part_ml + (size_t(cur_u) * slots_per_unit + c) * 16;
+        // the run's other chunks carry no partial of their own (for this group)
+        for (uint32_t c = seg_first + 1 + gtid / 8; c <= seg_last; c += kGroupThreads / 8) {
+            float* mc = part_ml + slot_of(cur_u, c, grp) * 16;
             mc[(gtid % 8) * 2] = -INFINITY;
             mc[(gtid % 8) * 2 + 1] = 0.0f;
         }
         // ---- completion counting; the last contributor merges ------------------
         __threadfence();
         group_sync(grp);
-        const uint32_t total = chunk_base[cur_u + 1] - chunk_base[cur_u];
+        const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
         if (gtid == 0) {
-            const uint32_t mine = (seg_last - seg_first) / kGroups + 1;
+            const uint32_t mine = seg_last - seg_first + 1;
             const uint32_t done = atomicAdd(unit_done + cur_u, mine) + mine;
-            gs.flag = done == total ? 1u : 0u;
-            if (done == total) unit_done[cur_u] = 0u;  // re-arm for the next step
+            gs.flag = done == kGroups * nch ? 1u : 0u;
+            if (done == kGroups * nch) unit_done[cur_u] = 0u;  // re-arm for the next step
         }
         group_sync(grp);
         if (gs.flag) {
             __threadfence();
             const UnitDesc du = L.desc[cur_u];
-            const float* mlu = part_ml + size_t(cur_u) * slots_per_unit * 16;
+            const float* mlu = part_ml + slot_of(cur_u, 0, 0) * 16;
+            const uint32_t nslots = nch * kGroups;
             for (uint32_t h = wg; h < G; h += kGroupThreads / 32) {
                 float M = -INFINITY;
-                for (uint32_t c = lane; c < total; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
+                for (uint32_t c = lane; c < nslots; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
                 constexpr int PER = D / 32;
@@ -338,12 +344,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
                 for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
                 float lsum2 = 0.0f;
-                for (uint32_t c = 0; c < total; ++c) {
+                for (uint32_t c = 0; c < nslots; ++c) {
                     const float m = __ldcg(mlu + c * 16 + h * 2);
                     if (m == -INFINITY) continue;
                     const float wgt = exp2f(m - M);
                     lsum2 += wgt * __ldcg(mlu + c * 16 + h * 2 + 1);
-                    const float* pc = part_o + ((size_t(cur_u) * slots_per_unit + c) * 8 + h) * D;
+                    const float* pc = part_o + ((slot_of(cur_u, 0, 0) + c) * 8 + h) * D;
 #pragma unroll
                     for (int i = 0; i < PER; ++i) acc[i] += wgt * __ldcg(pc + lane + 32 * i);
                 }
@@ -355,8 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     };
 
-    for (uint32_t i = grp; w_begin + i < w_end; i += kGroups) {
-        const uint32_t stage = i % kStages, phase = (i / kStages) & 1u;
+    uint32_t stage = 0, phase = 0;
+    for (uint32_t w = w_begin; w < w_end; ++w) {
         mbar_wait(smem_u32(&sh.full[stage]), phase);
         const StageMeta& mt = sh.meta[stage];
         const uint32_t u = mt.unit;
@@ -381,10 +387,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         const uint32_t v_base = k_base + TB;
         const bool any_invalid = mt.any_invalid != 0;
         if (any_invalid) {
-            // zero the V rows that carry no token: stale or uninitialised smem could
-            // hold NaN/Inf, and 0 * NaN would poison the PV product
-            for (uint32_t e = gtid; e < kRows * (D / 8); e += kGroupThreads) {
-                const uint32_t row = e / (D / 8), ch = e % (D / 8);
+            // zero this group's V rows that carry no token: stale or uninitialised smem
+            // could hold NaN/Inf, and 0 * NaN would poison the PV product
+            for (uint32_t e = gtid; e < kGroupRows * (D / 8); e += kGroupThreads) {
+                const uint32_t row = row0 + e / (D / 8), ch = e % (D / 8);
                 if ((row >> ns_log) >= mt.valid[row & (NS - 1)]) {
                     unsigned char* p = smem + stage * 2 * TB + TB + row_off(row) + ch * 16;
                     *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
@@ -393,36 +399,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             group_sync(grp);
         }
 
-        // S^T = K Q^T: warp wg owns logical rows [32wg, 32wg+32)
-        float s[2][4];
-#pragma unroll
-        for (int m = 0; m < 2; ++m) s[m][0] = s[m][1] = s[m][2] = s[m][3] = 0.0f;
+        // S^T = K Q^T: warp wg owns logical rows row0 + [16wg, 16wg+16)
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
-#pragma unroll
-            for (int m = 0; m < 2; ++m) {
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4(k_base + qk_off[m] + ks * 32, a0, a1, a2, a3);
-                mma_bf16(s[m], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-            }
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(k_base + qk_off + ks * 32, a0, a1, a2, a3);
+            mma_bf16(s, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
         }
-        bool rv[2][2];
+        bool rv[2];
 #pragma unroll
-        for (int m = 0; m < 2; ++m)
+        for (int hh = 0; hh < 2; ++hh) rv[hh] = !any_invalid || rv_row[hh] < mt.valid[rv_slot[hh]];
+        float mx[2];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) rv[m][hh] = !any_invalid || rv_row[m][hh] < mt.valid[rv_slot[m][hh]];
-        float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int m = 0; m < 2; ++m)
-#pragma unroll
-            for (int hc = 0; hc < 2; ++hc) {
-                if (rv[m][0]) mx[hc] = fmaxf(mx[hc], s[m][hc]);
-                if (rv[m][1]) mx[hc] = fmaxf(mx[hc], s[m][2 + hc]);
-            }
-#pragma unroll
-        for (int hc = 0; hc < 2; ++hc)
+        for (int hc = 0; hc < 2; ++hc) {
+            mx[hc] = fmaxf(rv[0] ? s[hc] : -INFINITY, rv[1] ? s[2 + hc] : -INFINITY);
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) mx[hc] = fmaxf(mx[hc], __shfl_xor_sync(0xffffffffu, mx[hc], off));
+        }
         if (g == 0) {
             gs.red[0][wg][2 * t4] = mx[0];
             gs.red[0][wg][2 * t4 + 1] = mx[1];
@@ -443,13 +437,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 o[m][2 + hc] *= alpha;
             }
         }
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-            const uint32_t r0 = wg * 32 + m * 16 + g;
+        {
+            const uint32_t r0 = wg * 16 + g;  // row within the group's P tile
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
-                const float p0 = rv[m][0] ? exp2f(fmaf(s[m][hc], scale_log2, -mnew[hc])) : 0.0f;
-                const float p1 = rv[m][1] ? exp2f(fmaf(s[m][2 + hc], scale_log2, -mnew[hc])) : 0.0f;
+                const float p0 = rv[0] ? exp2f(fmaf(s[hc], scale_log2, -mnew[hc])) : 0.0f;
+                const float p1 = rv[1] ? exp2f(fmaf(s[2 + hc], scale_log2, -mnew[hc])) : 0.0f;
                 l_run[hc] += p0 + p1;
                 const int h = 2 * t4 + hc;
                 const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
@@ -461,9 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
         group_sync(grp);
 
-        // O^T += V^T P^T: warp wg owns channels [wg*D/4, (wg+1)*D/4)
+        // O^T += V^T P^T over the group's rows: warp wg owns channels [wg*D/4, (wg+1)*D/4)
 #pragma unroll
-        for (int ks = 0; ks < kRows / 16; ++ks) {
+        for (int ks = 0; ks < kGroupRows / 16; ++ks) {
             const uint16_t* pp0 = gs.p[0] + g * kPStride + ks * 16 + 2 * t4;
             const uint16_t* pp1 = gs.p[1] + g * kPStride + ks * 16 + 2 * t4;
             const uint32_t b00 = *reinterpret_cast<const uint32_t*>(pp0);
@@ -480,6 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
+        if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+        }
     }
     if (cur_u != 0xffffffffu) flush();
 }
