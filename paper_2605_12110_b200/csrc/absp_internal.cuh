@@ -62,11 +62,14 @@ struct LayerView {
 cudaError_t launch_build_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches);
 cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreItem* items,
                          uint32_t n_items, cudaStream_t s, int* launches);
-// Selected blocks resolved to pool pages, per unit: slot s = entry * (B/P) + page.
+// Selected blocks resolved to pool pages, laid out by global attention chunk:
+// unit u's slot s = entry * (B/P) + page lives at index chunk_base[u] * ns + s, so
+// chunk w's slots are [w * ns, (w + 1) * ns).
 struct PageList {
-    uint32_t* page;   // [units][stride] pool page id
-    uint16_t* valid;  // [units][stride] valid rows of the page (0 = empty slot)
-    uint32_t stride;  // slots per unit
+    uint32_t* page;               // head * pool_pages + pool page id
+    uint16_t* valid;              // valid rows of the page (0 = empty slot)
+    const uint32_t* chunk_base;   // [units + 1] first chunk of each unit (work list)
+    uint32_t ns;                  // page slots per chunk = kAttnChunkRows / P
 };
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,

@@ -75,9 +75,9 @@ struct DevBuf {
 // Device-side attention work list (see AttendWork).
 struct WorkList {
     DevBuf<uint32_t> chunk_unit, chunk_idx, chunk_base, unit_done;
-    DevBuf<uint32_t> page;    // resolved page list, [units][page_stride]
+    DevBuf<uint32_t> page;    // resolved page list, [n_work][ns] (see PageList)
     DevBuf<uint16_t> valid;
-    uint32_t n_work = 0, slots = 0, page_stride = 0;
+    uint32_t n_work = 0, slots = 0, ns = 0;
     void release() {
         chunk_unit.release();
         chunk_idx.release();
@@ -86,7 +86,7 @@ struct WorkList {
         page.release();
         valid.release();
     }
-    PageList pages() const { return PageList{page.p, valid.p, page_stride}; }
+    PageList pages() const { return PageList{page.p, valid.p, chunk_base.p, ns}; }
 };
 
 struct Layer {
@@ -206,18 +206,19 @@ absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t c
     }
     wl.n_work = base.back();
     wl.slots = slots;
-    wl.page_stride = slots * (kAttnChunkRows / P);  // page slots per unit
+    wl.ns = kAttnChunkRows / P;  // page slots per chunk
+    const size_t n_slots = size_t(wl.n_work) * wl.ns;
     ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
     ABSP_CUDA(wl.chunk_idx.ensure(idx_of.size()));
     ABSP_CUDA(wl.chunk_base.ensure(base.size()));
     ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
-    ABSP_CUDA(wl.page.ensure(l.desc.size() * size_t(wl.page_stride)));
-    ABSP_CUDA(wl.valid.ensure(l.desc.size() * size_t(wl.page_stride)));
+    ABSP_CUDA(wl.page.ensure(n_slots));
+    ABSP_CUDA(wl.valid.ensure(n_slots));
     ABSP_CUDA(cudaMemcpy(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
-    ABSP_CUDA(cudaMemset(wl.valid.p, 0, l.desc.size() * size_t(wl.page_stride) * 2));
+    ABSP_CUDA(cudaMemset(wl.valid.p, 0, n_slots * 2));
     ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(slots) * kAttnGroups * 8 * D));
     ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(slots) * kAttnGroups * 16));
     return ABSP_OK;

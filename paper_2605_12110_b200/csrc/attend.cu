@@ -173,35 +173,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 
     if (warp == kConsumers / 32) {
         // ============================ producer ================================
-        // The page list (resolved by the top-k kernel) of chunk w+1 is fetched while
-        // chunk w waits for a free stage, so the two dependent L2 round trips
-        // (chunk -> unit, unit -> pages) stay off the copy-issue path. Lane k*32+l
-        // owns page slot k*32+l (NS <= 128 slots -> up to 4 per lane).
+        // The page list (resolved by the top-k kernel, laid out by global chunk index)
+        // of chunk w+2 is fetched while chunk w waits for a free stage: one round trip
+        // of independent loads, two chunks ahead of the copy issue. Lane k*32+l owns
+        // page slot k*32+l (NS <= 128 slots -> up to 4 per lane).
         constexpr int SPL = kMaxSlots / 32;
-        uint32_t nu = 0, ncx = 0, ngp[SPL], nvl[SPL];
-        auto fetch = [&](uint32_t w) {
+        struct Pref {
+            uint32_t u, c, gp[SPL], vl[SPL];
+        };
+        auto fetch = [&](uint32_t w, Pref& f) {
             if (w >= w_end) return;
-            nu = __ldg(chunk_unit + w);
-            ncx = __ldg(chunk_idx + w);
-            const size_t base = size_t(nu) * pages.stride + size_t(ncx) * NS;
+            f.u = __ldg(chunk_unit + w);
+            f.c = __ldg(chunk_idx + w);
+            const size_t base = size_t(w) * NS;
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
                 const uint32_t s = k * 32 + lane;
-                ngp[k] = s < NS ? __ldcg(pages.page + base + s) : 0u;
-                nvl[k] = s < NS ? __ldcg(pages.valid + base + s) : 0u;
+                f.gp[k] = s < NS ? __ldcg(pages.page + base + s) : 0u;
+                f.vl[k] = s < NS ? __ldcg(pages.valid + base + s) : 0u;
             }
         };
-        fetch(w_begin);
+        Pref f0{}, f1{};
+        fetch(w_begin, f0);
+        fetch(w_begin + 1, f1);
         uint32_t stage = 0, phase = 0;
         for (uint32_t w = w_begin; w < w_end; ++w) {
-            const uint32_t u = nu, c = ncx;
+            const uint32_t u = f0.u, c = f0.c;
             uint32_t gp[SPL], vl[SPL];
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
-                gp[k] = ngp[k];
-                vl[k] = nvl[k];
+                gp[k] = f0.gp[k];
+                vl[k] = f0.vl[k];
             }
-            fetch(w + 1);
+            f0 = f1;
+            fetch(w + 2, f1);
             mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
             StageMeta& mt = sh.meta[stage];
             const uint32_t kdst = smem_base + stage * 2 * TB;

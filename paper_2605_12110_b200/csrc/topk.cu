@@ -94,8 +94,9 @@ __device__ __forceinline__ void resolve_pages(const LayerView& L, const UnitDesc
     const uint32_t slot_end = ((sel_total + E - 1) / E * E) << ppb_log;
     const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
     const uint32_t head_base = du.head * uint32_t(L.pool_pages);
-    uint32_t* pg = pages.page + size_t(u) * pages.stride;
-    uint16_t* vl = pages.valid + size_t(u) * pages.stride;
+    const size_t base = size_t(pages.chunk_base[u]) * pages.ns;
+    uint32_t* pg = pages.page + base;
+    uint16_t* vl = pages.valid + base;
     __syncthreads();  // `out` (global) written by this block is visible block-wide
     for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
         const uint32_t e = s >> ppb_log, pp = s & ((1u << ppb_log) - 1u);
@@ -585,6 +586,7 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
     const uint32_t slot_end = ((cap + E - 1) / E) * E * ppb;
     const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
     const uint32_t head_base = du.head * uint32_t(L.pool_pages);
+    const size_t base = size_t(pages.chunk_base[u]) * pages.ns;
     for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
         const uint32_t e = s / ppb, pp = s % ppb;
         uint32_t v = 0, page = 0;
@@ -595,8 +597,8 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
                 page = head_base + __ldg(pt + t0 / L.P);
             }
         }
-        pages.page[size_t(u) * pages.stride + s] = page;
-        pages.valid[size_t(u) * pages.stride + s] = uint16_t(v);
+        pages.page[base + s] = page;
+        pages.valid[base + s] = uint16_t(v);
     }
 }
 
