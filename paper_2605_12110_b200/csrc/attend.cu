@@ -78,6 +78,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void group_sync(uint32_t grp) {  // named barrier 1 + grp
     asm volatile("bar.sync %0, %1;\n" ::"r"(grp + 1), "n"(kGroupThreads) : "memory");
 }
@@ -110,6 +115,7 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
 }
 
 struct StageMeta {
+    __align__(16) uint16_t q[8 * 128];  // the chunk's unit's G query rows (bf16)
     uint32_t unit;
     uint32_t chunk;
     uint32_t any_invalid;       // some row of the chunk carries no token
@@ -223,7 +229,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 mt.unit = u;
                 mt.chunk = c;
                 mt.any_invalid = invalid ? 1u : 0u;
-                mbar_expect_tx(full, bytes);
+                // the unit's G query rows ride along (units are b-major: q row block
+                // of unit u = b*H + h starts at u * G * D)
+                mbar_expect_tx(full, bytes + L.G * D * 2);
+                bulk_g2s(smem_u32(mt.q), q + size_t(u) * L.G * D, L.G * D * 2, full);
             }
             __syncwarp();
 #pragma unroll
@@ -282,8 +291,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         return (size_t(unit) * slots_per_unit + chunk) * kGroups + gr;
     };
 
-    // Emit this group's partial of (cur_u, chunks seg_first..seg_last); the
-    // contributor completing the unit merges all of the unit's partials into `out`.
+    // LSE merge of all partials of unit mu into `out` (one warp per query head).
+    // Lane-parallel over partial slots: weights exp2(m - M) are computed for 32
+    // slots at a time, and only slots holding a real partial (weight != 0) are read.
+    auto merge = [&](uint32_t mu) {
+        const uint32_t nslots = (chunk_base[mu + 1] - chunk_base[mu]) * kGroups;
+        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16;
+        const float* pou = part_o + slot_of(mu, 0, 0) * 8 * D;
+        constexpr int PER = D / 32;
+        for (uint32_t h = wg; h < G; h += kGroupThreads / 32) {
+            float M = -INFINITY;
+            for (uint32_t c = lane; c < nslots; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            float acc[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
+            float lsum = 0.0f;
+            for (uint32_t c0 = 0; c0 < nslots; c0 += 32) {
+                const uint32_t c = c0 + lane;
+                const float m = c < nslots ? __ldcg(mlu + c * 16 + h * 2) : -INFINITY;
+                const float wgt = m == -INFINITY ? 0.0f : exp2f(m - M);
+                lsum += wgt == 0.0f ? 0.0f : wgt * __ldcg(mlu + c * 16 + h * 2 + 1);
+                for (uint32_t live = __ballot_sync(0xffffffffu, wgt != 0.0f); live; live &= live - 1) {
+                    const uint32_t src = __ffs(live) - 1;
+                    const float wc = __shfl_sync(0xffffffffu, wgt, src);
+                    const float* pc = pou + ((c0 + src) * 8 + h) * D;
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) acc[i] += wc * __ldcg(pc + lane + 32 * i);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+            const float inv = 1.0f / lsum;
+            float* dst = out + (size_t(mu) * G + h) * D;  // out is [b][h*G + g][d], u = b*H + h
+#pragma unroll
+            for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
+        }
+    };
+
+    // Units this group completed: merged after the chunk loop so a merge never
+    // stalls the pipeline mid-range (a full list merges immediately).
+    constexpr int kMaxPend = 4;
+    uint32_t pend[kMaxPend];
+    int npend = 0;
+
+    // Emit this group's partial of (cur_u, chunks seg_first..seg_last) and count
+    // the chunks; the contributor completing the unit schedules its merge.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
@@ -323,45 +377,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             mc[(gtid % 8) * 2] = -INFINITY;
             mc[(gtid % 8) * 2 + 1] = 0.0f;
         }
-        // ---- completion counting; the last contributor merges ------------------
-        __threadfence();
+        // ---- completion counting (release: the partials above become visible to
+        // the contributor that completes the unit, which acquires) ---------------
         group_sync(grp);
-        const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
         if (gtid == 0) {
+            const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
             const uint32_t mine = seg_last - seg_first + 1;
-            const uint32_t done = atomicAdd(unit_done + cur_u, mine) + mine;
+            const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
             gs.flag = done == kGroups * nch ? 1u : 0u;
             if (done == kGroups * nch) unit_done[cur_u] = 0u;  // re-arm for the next step
         }
         group_sync(grp);
         if (gs.flag) {
-            __threadfence();
-            const UnitDesc du = L.desc[cur_u];
-            const float* mlu = part_ml + slot_of(cur_u, 0, 0) * 16;
-            const uint32_t nslots = nch * kGroups;
-            for (uint32_t h = wg; h < G; h += kGroupThreads / 32) {
-                float M = -INFINITY;
-                for (uint32_t c = lane; c < nslots; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-                constexpr int PER = D / 32;
-                float acc[PER];
-#pragma unroll
-                for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
-                float lsum2 = 0.0f;
-                for (uint32_t c = 0; c < nslots; ++c) {
-                    const float m = __ldcg(mlu + c * 16 + h * 2);
-                    if (m == -INFINITY) continue;
-                    const float wgt = exp2f(m - M);
-                    lsum2 += wgt * __ldcg(mlu + c * 16 + h * 2 + 1);
-                    const float* pc = part_o + ((slot_of(cur_u, 0, 0) + c) * 8 + h) * D;
-#pragma unroll
-                    for (int i = 0; i < PER; ++i) acc[i] += wgt * __ldcg(pc + lane + 32 * i);
-                }
-                const float inv = 1.0f / lsum2;
-                float* dst = out + (size_t(du.seq) * L.H * G + size_t(du.head) * G + h) * D;
-#pragma unroll
-                for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
+            if (npend == kMaxPend) {
+                merge(cur_u);
+            } else {
+                pend[npend++] = cur_u;
             }
         }
     };
@@ -379,12 +410,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             l_run[0] = l_run[1] = 0.0f;
 #pragma unroll
             for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
-            const UnitDesc du = L.desc[u];
-            const uint16_t* qrow = q + (size_t(du.seq) * L.H * G + size_t(du.head) * G + g) * D;
+            // Q^T fragments (B operand) from the q rows staged with the chunk
+            const uint16_t* qrow = mt.q + g * D;
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
-                qb[ks][0] = g < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4)) : 0u;
-                qb[ks][1] = g < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4)) : 0u;
+                qb[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+                qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
             }
         }
         seg_last = mt.chunk;
@@ -484,6 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     }
     if (cur_u != 0xffffffffu) flush();
+    for (int i = 0; i < npend; ++i) merge(pend[i]);
 }
 
 }  // namespace

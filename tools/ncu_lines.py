@@ -21,7 +21,8 @@ def sass_rows(rep):
     rows = list(csv.reader(io.StringIO(out)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hi]
-    si = h.index("Warp Stall Sampling (All Samples)")
+    col = os.environ.get("NCU_REASON", "Warp Stall Sampling (All Samples)")
+    si = h.index(col)
     ii = h.index("Instructions Executed")
     res = []
     for r in rows[hi + 1:]:
