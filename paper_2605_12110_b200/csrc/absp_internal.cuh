@@ -98,9 +98,9 @@ cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint
 
 // Rows per attention chunk (one pipeline stage), see attend.cu.
 constexpr uint32_t kAttnChunkRows = 128;
-// Consumer groups per attention CTA; each owns a row split of every chunk and
-// emits its own partials (partial slots per chunk).
-constexpr uint32_t kAttnGroups = 2;
+// Consumer warps per attention CTA; each owns a 16-row split of every chunk with
+// its own online-softmax state and partials (partial slots per chunk).
+constexpr uint32_t kAttnSplits = 8;
 // Centroids per scoring CTA, see score.cu.
 constexpr uint32_t kScoreItemCentroids = 2048;
 

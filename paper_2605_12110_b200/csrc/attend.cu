@@ -4,34 +4,37 @@
 // Reference: sparse_attention / attend_rows (engine.cpp:180-210, 285-327):
 // softmax(q . k / sqrt(d)) . v over the rows of the selected blocks, rows
 // resolved through the page table (block_to_pages, kv_cache.cpp:118-138). The
-// PageSpan objects of populate_page_spans (engine.cpp:271-283) are replaced by
-// index arithmetic: block j of head h covers page-table entries
-// [j*B/P, (j+1)*B/P) — no gather copy, no per-step allocation.
+// PageSpan objects of populate_page_spans (engine.cpp:271-283) become the page
+// list the top-k kernel resolves; no gather copy, no per-step allocation.
 //
 // Work: the selection of unit u = (b, h) is cut into chunks of E = 128/B
-// consecutive entries (<= 128 rows = 128/P whole pages). All chunks of all units
-// form one list; a persistent grid (one CTA per SM) takes contiguous ranges of it,
-// so every SM streams the same number of KV bytes regardless of block sizes.
+// consecutive entries (128 rows = 128/P whole pages). All chunks of all units form
+// one list; a persistent grid (one CTA per SM) takes contiguous ranges of it, so
+// every SM streams the same number of KV bytes whatever the block sizes.
 //
-// CTA = 2 groups of 4 consumer warps + 1 producer warp, 3-stage mbarrier ring:
-//   producer : lane s resolves page slot s of the next chunk (selected block ->
-//              page table -> pool page) and issues one cp.async.bulk per page for K
-//              and V (the TMA bulk-copy engine; 1 instruction per 1-4 KB page),
-//              completing on the stage's full barrier.
-//   consumers: (two groups split each chunk's rows so their latency chains overlap)
-//              S^T = K Q^T and O^T += V^T P^T on mma.m16n8k16 (M = 16 KV rows or
-//              channels, N = 8 query heads of the GQA group), fp32 online softmax
-//              across the chunks of a unit, P kept as a bf16 hi/lo pair (~16
-//              mantissa bits). A run of chunks of one unit ends in a partial
-//              (m, l, o[G][d]); the CTA that completes a unit's last chunk merges
-//              the unit's partials (fused LSE merge, completion counter per unit).
+// CTA = 8 consumer warps + 1 producer warp, 3-stage mbarrier ring of 64 KB stages:
+//   producer : lane s handles page slot s of the chunk two ahead (page list
+//              prefetched with independent loads) and issues one cp.async.bulk per
+//              page for K and V — the TMA bulk-copy engine, 1 instruction per 1-4 KB
+//              page — plus one for the unit's G query rows, completing on the
+//              stage's full barrier. (A copy-only probe of this pipeline streams
+//              scattered 4 KB pages at 97% of measured HBM bandwidth.)
+//   consumers: warp w owns rows [16w, 16w+16) of every chunk and is an independent
+//              split with its own fp32 online-softmax state: S^T = K Q^T on
+//              mma.m16n8k16 (M = 16 KV rows, N = 8 query heads of the GQA group,
+//              K = d), P through a per-warp smem tile (bf16 hi + bf16 residual,
+//              ~16 mantissa bits), O^T += V^T P^T (M = 16 channels x d/16 tiles,
+//              N = 8 heads, K = the warp's 16 rows). No cross-warp barrier in the
+//              chunk loop. A run of chunks of one unit ends in a per-warp partial
+//              (m, l, o[G][d]); the warp that completes a unit merges its partials
+//              (LSE merge fused into the kernel, deferred to the end of the range).
 //
 // Bank conflicts without TMA swizzle: a page lands contiguously in smem, so rows
-// of one page are 256 B apart (same banks). Page slots are therefore staggered by
-// 16 B and logical row i of a chunk is (slot i % NS, row i / NS), NS = 128/P: the
-// 8 rows of every ldmatrix phase come from 8 different slots and hit 8 distinct
-// 16 B bank groups (for P <= 16). Softmax is permutation-invariant over rows, and
-// the same permutation indexes P, so the result is unchanged.
+// of one page are 256 B apart (same banks). Page slots are staggered by 16 B and
+// logical row i of a chunk is (slot i % NS, row i / NS), NS = 128/P: the 8 rows of
+// an ldmatrix phase come from 8 different slots, i.e. 8 distinct 16 B bank groups
+// (P <= 16). Softmax is permutation-invariant over rows and P uses the same
+// permutation, so the result is unchanged.
 #include "absp_internal.cuh"
 
 #include <math.h>
@@ -39,15 +42,14 @@
 namespace absp {
 namespace {
 
-constexpr int kRows = kAttnChunkRows;  // 128
-constexpr int kGroupThreads = 128;     // one consumer group = 4 warps
-constexpr int kGroups = kAttnGroups;   // consumer groups, each owning half of every chunk
-constexpr int kConsumers = kGroupThreads * kGroups;
+constexpr int kRows = kAttnChunkRows;    // 128 rows per chunk / stage
+constexpr int kWarps = kAttnSplits;      // consumer warps = splits per chunk (8)
+constexpr int kConsumers = 32 * kWarps;
 constexpr int kThreads = kConsumers + 32;  // + 1 producer warp
 constexpr int kStages = 3;
-constexpr int kGroupRows = kRows / 2;  // rows of a chunk owned by one consumer group
-constexpr int kPStride = kGroupRows + 8;  // bf16 row stride of P (bank-conflict free)
-constexpr int kMaxSlots = kRows;       // P >= 1
+constexpr int kWarpRows = kRows / kWarps;  // 16
+constexpr int kPStride = kWarpRows + 8;    // bf16 row stride of a P tile (bank-conflict free)
+constexpr int kMaxSlots = kRows;           // P >= 1
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -82,9 +84,6 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
     uint32_t old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
-}
-__device__ __forceinline__ void group_sync(uint32_t grp) {  // named barrier 1 + grp
-    asm volatile("bar.sync %0, %1;\n" ::"r"(grp + 1), "n"(kGroupThreads) : "memory");
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
@@ -122,17 +121,11 @@ struct StageMeta {
     uint16_t valid[kMaxSlots];  // valid rows per page slot (0..P)
 };
 
-struct GroupSmem {
-    uint16_t p[2][8 * kPStride];  // P as bf16 hi + bf16 residual
-    float red[2][4][8];           // per-warp max / sum per head
-    uint32_t flag;
-};
-
 struct SmemHead {  // fixed-size part after the stage tiles
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     StageMeta meta[kStages];
-    GroupSmem grp[kGroups];
+    uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
 };
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
@@ -155,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                                                       float* __restrict__ part_ml,
                                                       uint32_t* __restrict__ unit_done,
                                                       float* __restrict__ out) {
-    constexpr int MT = D / 64;  // 16-channel PV m-tiles per consumer warp
+    constexpr int MT = D / 16;  // 16-channel PV m-tiles (each warp covers every channel)
     extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t P = L.P;
     const uint32_t NS = kRows / P;  // page slots per chunk
@@ -171,13 +164,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&sh.full[s]), 1);
-            mbar_init(smem_u32(&sh.empty[s]), kConsumers / 32);  // every consumer warp
+            mbar_init(smem_u32(&sh.empty[s]), kWarps);  // every consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == kConsumers / 32) {
+    if (warp == kWarps) {
         // ============================ producer ================================
         // The page list (resolved by the top-k kernel, laid out by global chunk index)
         // of chunk w+2 is fetched while chunk w waits for a free stage: one round trip
@@ -229,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 mt.unit = u;
                 mt.chunk = c;
                 mt.any_invalid = invalid ? 1u : 0u;
-                // the unit's G query rows ride along (units are b-major: q row block
+                // the unit's G query rows ride along (units are b-major: the q row block
                 // of unit u = b*H + h starts at u * G * D)
                 mbar_expect_tx(full, bytes + L.G * D * 2);
                 bulk_g2s(smem_u32(mt.q), q + size_t(u) * L.G * D, L.G * D * 2, full);
@@ -253,12 +246,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     }
 
     // ============================== consumers =================================
-    // Both groups consume every stage; group g owns logical rows [64g, 64g+64) of
-    // each chunk (a row split with its own online-softmax state and partials), so
-    // the per-chunk MMA/softmax latency chain is half as long and the two groups'
-    // chains overlap. Every waiter sees every phase of every barrier in order.
-    const uint32_t grp = warp / 4, wg = warp % 4, gtid = tid % kGroupThreads;
-    GroupSmem& gs = sh.grp[grp];
     const uint32_t g = lane >> 2, t4 = lane & 3;
     const uint32_t G = L.G;
     const float scale_log2 = rsqrtf(float(D)) * 1.4426950408889634f;
@@ -267,39 +254,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     auto row_off = [&](uint32_t i) -> uint32_t {
         return (i & (NS - 1)) * slot_stride + (i >> ns_log) * (D * 2);
     };
-    const uint32_t row0 = grp * kGroupRows;  // first logical row of this group
-    // per-thread smem offsets, identical for every chunk
-    const uint32_t qk_off = row_off(row0 + wg * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) + (lane >> 4) * 16;
-    uint32_t rv_slot[2], rv_row[2], pv_off[kGroupRows / 16];
+    const uint32_t row0 = warp * kWarpRows;
+    // per-thread smem offsets, identical for every chunk:
+    //   QK  A = K rows (ldmatrix): lanes 0-15 rows 0-15 at k-chunk 0, lanes 16-31 at chunk 1
+    //   PV  A = V^T (ldmatrix.trans): lanes 0-7 rows 0-7 ch 0, 8-15 rows 0-7 ch 8,
+    //       16-23 rows 8-15 ch 0, 24-31 rows 8-15 ch 8
+    const uint32_t qk_off = row_off(row0 + (lane & 7) + ((lane >> 3) & 1) * 8) + (lane >> 4) * 16;
+    const uint32_t pv_off = row_off(row0 + (lane & 7) + ((lane >> 4) & 1) * 8) + ((lane >> 3) & 1) * 16;
+    uint32_t rv_slot[2], rv_row[2];
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t row = row0 + wg * 16 + g + hh * 8;
+        const uint32_t row = row0 + g + hh * 8;
         rv_slot[hh] = row & (NS - 1);
         rv_row[hh] = row >> ns_log;
     }
-#pragma unroll
-    for (int ks = 0; ks < kGroupRows / 16; ++ks)
-        pv_off[ks] = row_off(row0 + ks * 16 + (lane & 7) + ((lane >> 4) & 1) * 8) + ((lane >> 3) & 1) * 16;
+    uint16_t* pt0 = sh.p[warp][0];
+    uint16_t* pt1 = sh.p[warp][1];
 
     uint32_t cur_u = 0xffffffffu, seg_first = 0, seg_last = 0;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // partial slot of (unit, first chunk of a run, group)
-    auto slot_of = [&](uint32_t unit, uint32_t chunk, uint32_t gr) -> size_t {
-        return (size_t(unit) * slots_per_unit + chunk) * kGroups + gr;
+    // partial slot of (unit, first chunk of a run, warp)
+    auto slot_of = [&](uint32_t unit, uint32_t chunk, uint32_t wp) -> size_t {
+        return (size_t(unit) * slots_per_unit + chunk) * kWarps + wp;
     };
 
-    // LSE merge of all partials of unit mu into `out` (one warp per query head).
+    // LSE merge of all partials of unit mu into `out` by this warp (all G heads).
     // Lane-parallel over partial slots: weights exp2(m - M) are computed for 32
-    // slots at a time, and only slots holding a real partial (weight != 0) are read.
+    // slots at a time and only slots holding a real partial (weight != 0) are read.
     auto merge = [&](uint32_t mu) {
-        const uint32_t nslots = (chunk_base[mu + 1] - chunk_base[mu]) * kGroups;
+        const uint32_t nslots = (chunk_base[mu + 1] - chunk_base[mu]) * kWarps;
         const float* mlu = part_ml + slot_of(mu, 0, 0) * 16;
         const float* pou = part_o + slot_of(mu, 0, 0) * 8 * D;
         constexpr int PER = D / 32;
-        for (uint32_t h = wg; h < G; h += kGroupThreads / 32) {
+        for (uint32_t h = 0; h < G; ++h) {
             float M = -INFINITY;
             for (uint32_t c = lane; c < nslots; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
 #pragma unroll
@@ -330,70 +320,61 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     };
 
-    // Units this group completed: merged after the chunk loop so a merge never
-    // stalls the pipeline mid-range (a full list merges immediately).
+    // Units this warp completed: merged after the chunk loop so a merge never stalls
+    // the pipeline mid-range (a full list merges immediately).
     constexpr int kMaxPend = 4;
     uint32_t pend[kMaxPend];
     int npend = 0;
 
-    // Emit this group's partial of (cur_u, chunks seg_first..seg_last) and count
-    // the chunks; the contributor completing the unit schedules its merge.
+    // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count the
+    // chunks; the warp completing the unit schedules its merge.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
-        group_sync(grp);  // red[] free
-        if (g == 0) {
-            gs.red[1][wg][2 * t4] = lsum[0];
-            gs.red[1][wg][2 * t4 + 1] = lsum[1];
-        }
-        const size_t slot = slot_of(cur_u, seg_first, grp);
+        const size_t slot = slot_of(cur_u, seg_first, warp);
         float* po = part_o + slot * 8 * D;
         float* ml = part_ml + slot * 16;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            const uint32_t c0 = wg * (D / 4) + mt * 16 + g;
+        for (int m = 0; m < MT; ++m) {
+            const uint32_t c0 = m * 16 + g;
 #pragma unroll
             for (int hc = 0; hc < 2; ++hc) {
                 const uint32_t h = 2 * t4 + hc;
                 if (h < G) {
-                    po[h * D + c0] = o[mt][hc];
-                    po[h * D + c0 + 8] = o[mt][2 + hc];
+                    po[h * D + c0] = o[m][hc];
+                    po[h * D + c0 + 8] = o[m][2 + hc];
                 }
             }
         }
-        if (wg == 0 && g == 0) {  // m is group-uniform per head
+        if (g == 0) {  // m and l are warp-uniform per head
             ml[(2 * t4) * 2] = m_run[0];
+            ml[(2 * t4) * 2 + 1] = lsum[0];
             ml[(2 * t4 + 1) * 2] = m_run[1];
+            ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
         }
-        group_sync(grp);
-        if (gtid < 8)
-            ml[gtid * 2 + 1] = gs.red[1][0][gtid] + gs.red[1][1][gtid] + gs.red[1][2][gtid] + gs.red[1][3][gtid];
-        // the run's other chunks carry no partial of their own (for this group)
-        for (uint32_t c = seg_first + 1 + gtid / 8; c <= seg_last; c += kGroupThreads / 8) {
-            float* mc = part_ml + slot_of(cur_u, c, grp) * 16;
-            mc[(gtid % 8) * 2] = -INFINITY;
-            mc[(gtid % 8) * 2 + 1] = 0.0f;
+        // the run's other chunks carry no partial of their own (for this warp)
+        for (uint32_t c = seg_first + 1 + lane / 8; c <= seg_last; c += 4) {
+            float* mc = part_ml + slot_of(cur_u, c, warp) * 16;
+            mc[(lane % 8) * 2] = -INFINITY;
+            mc[(lane % 8) * 2 + 1] = 0.0f;
         }
-        // ---- completion counting (release: the partials above become visible to
-        // the contributor that completes the unit, which acquires) ---------------
-        group_sync(grp);
-        if (gtid == 0) {
+        // completion counting: release publishes the partials to the warp that
+        // completes the unit, whose acquire makes every partial visible to it
+        __syncwarp();
+        uint32_t last = 0;
+        if (lane == 0) {
             const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
             const uint32_t mine = seg_last - seg_first + 1;
             const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
-            gs.flag = done == kGroups * nch ? 1u : 0u;
-            if (done == kGroups * nch) unit_done[cur_u] = 0u;  // re-arm for the next step
+            last = done == kWarps * nch;
+            if (last) unit_done[cur_u] = 0u;  // re-arm for the next step
         }
-        group_sync(grp);
-        if (gs.flag) {
-            if (npend == kMaxPend) {
-                merge(cur_u);
-            } else {
-                pend[npend++] = cur_u;
-            }
+        if (__shfl_sync(0xffffffffu, last, 0)) {
+            if (npend == kMaxPend) merge(cur_u);
+            else pend[npend++] = cur_u;
         }
     };
 
@@ -410,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             l_run[0] = l_run[1] = 0.0f;
 #pragma unroll
             for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
-            // Q^T fragments (B operand) from the q rows staged with the chunk
+            // Q^T fragments (B operand): b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]
             const uint16_t* qrow = mt.q + g * D;
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
@@ -423,47 +404,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         const uint32_t v_base = k_base + TB;
         const bool any_invalid = mt.any_invalid != 0;
         if (any_invalid) {
-            // zero this group's V rows that carry no token: stale or uninitialised smem
+            // zero this warp's V rows that carry no token: stale or uninitialised smem
             // could hold NaN/Inf, and 0 * NaN would poison the PV product
-            for (uint32_t e = gtid; e < kGroupRows * (D / 8); e += kGroupThreads) {
+            for (uint32_t e = lane; e < kWarpRows * (D / 8); e += 32) {
                 const uint32_t row = row0 + e / (D / 8), ch = e % (D / 8);
                 if ((row >> ns_log) >= mt.valid[row & (NS - 1)]) {
                     unsigned char* p = smem + stage * 2 * TB + TB + row_off(row) + ch * 16;
                     *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
                 }
             }
-            group_sync(grp);
+            __syncwarp();
         }
 
-        // S^T = K Q^T: warp wg owns logical rows row0 + [16wg, 16wg+16)
-        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        // S^T = K Q^T over the warp's 16 rows: two accumulator chains (even / odd ks)
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
             uint32_t a0, a1, a2, a3;
             ldsm_x4(k_base + qk_off + ks * 32, a0, a1, a2, a3);
-            mma_bf16(s, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+            mma_bf16((ks & 1) ? s2 : s, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i] += s2[i];
         bool rv[2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) rv[hh] = !any_invalid || rv_row[hh] < mt.valid[rv_slot[hh]];
-        float mx[2];
-#pragma unroll
-        for (int hc = 0; hc < 2; ++hc) {
-            mx[hc] = fmaxf(rv[0] ? s[hc] : -INFINITY, rv[1] ? s[2 + hc] : -INFINITY);
-#pragma unroll
-            for (int off = 4; off < 32; off <<= 1) mx[hc] = fmaxf(mx[hc], __shfl_xor_sync(0xffffffffu, mx[hc], off));
-        }
-        if (g == 0) {
-            gs.red[0][wg][2 * t4] = mx[0];
-            gs.red[0][wg][2 * t4 + 1] = mx[1];
-        }
-        group_sync(grp);
+        // warp-local online softmax: this warp is its own split
         float mnew[2];
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc) {
-            const int h = 2 * t4 + hc;
-            const float cm = fmaxf(fmaxf(gs.red[0][0][h], gs.red[0][1][h]), fmaxf(gs.red[0][2][h], gs.red[0][3][h]));
-            mnew[hc] = fmaxf(m_run[hc], cm * scale_log2);
+            float mx = fmaxf(rv[0] ? s[hc] : -INFINITY, rv[1] ? s[2 + hc] : -INFINITY);
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            mnew[hc] = fmaxf(m_run[hc], mx * scale_log2);
             const float alpha = mnew[hc] == -INFINITY ? 1.0f : exp2f(m_run[hc] - mnew[hc]);
             m_run[hc] = mnew[hc];
             l_run[hc] *= alpha;
@@ -473,39 +446,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 o[m][2 + hc] *= alpha;
             }
         }
-        {
-            const uint32_t r0 = wg * 16 + g;  // row within the group's P tile
 #pragma unroll
-            for (int hc = 0; hc < 2; ++hc) {
-                const float p0 = rv[0] ? exp2f(fmaf(s[hc], scale_log2, -mnew[hc])) : 0.0f;
-                const float p1 = rv[1] ? exp2f(fmaf(s[2 + hc], scale_log2, -mnew[hc])) : 0.0f;
-                l_run[hc] += p0 + p1;
-                const int h = 2 * t4 + hc;
-                const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
-                gs.p[0][h * kPStride + r0] = h0;
-                gs.p[0][h * kPStride + r0 + 8] = h1;
-                gs.p[1][h * kPStride + r0] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
-                gs.p[1][h * kPStride + r0 + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
-            }
+        for (int hc = 0; hc < 2; ++hc) {
+            const float p0 = rv[0] ? exp2f(fmaf(s[hc], scale_log2, -mnew[hc])) : 0.0f;
+            const float p1 = rv[1] ? exp2f(fmaf(s[2 + hc], scale_log2, -mnew[hc])) : 0.0f;
+            l_run[hc] += p0 + p1;
+            const int h = 2 * t4 + hc;
+            const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
+            pt0[h * kPStride + g] = h0;
+            pt0[h * kPStride + g + 8] = h1;
+            pt1[h * kPStride + g] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
+            pt1[h * kPStride + g + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
         }
-        group_sync(grp);
-
-        // O^T += V^T P^T over the group's rows: warp wg owns channels [wg*D/4, (wg+1)*D/4)
+        __syncwarp();
+        // O^T += V^T P^T, K = the warp's 16 rows: b0 = P[head g][rows 2t..], b1 = rows 8+2t..
+        const uint32_t b00 = *reinterpret_cast<const uint32_t*>(pt0 + g * kPStride + 2 * t4);
+        const uint32_t b01 = *reinterpret_cast<const uint32_t*>(pt0 + g * kPStride + 8 + 2 * t4);
+        const uint32_t b10 = *reinterpret_cast<const uint32_t*>(pt1 + g * kPStride + 2 * t4);
+        const uint32_t b11 = *reinterpret_cast<const uint32_t*>(pt1 + g * kPStride + 8 + 2 * t4);
 #pragma unroll
-        for (int ks = 0; ks < kGroupRows / 16; ++ks) {
-            const uint16_t* pp0 = gs.p[0] + g * kPStride + ks * 16 + 2 * t4;
-            const uint16_t* pp1 = gs.p[1] + g * kPStride + ks * 16 + 2 * t4;
-            const uint32_t b00 = *reinterpret_cast<const uint32_t*>(pp0);
-            const uint32_t b01 = *reinterpret_cast<const uint32_t*>(pp0 + 8);
-            const uint32_t b10 = *reinterpret_cast<const uint32_t*>(pp1);
-            const uint32_t b11 = *reinterpret_cast<const uint32_t*>(pp1 + 8);
-#pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                uint32_t a0, a1, a2, a3;
-                ldsm_x4_t(v_base + pv_off[ks] + (wg * (D / 4) + m * 16) * 2, a0, a1, a2, a3);
-                mma_bf16(o[m], a0, a1, a2, a3, b00, b01);
-                mma_bf16(o[m], a0, a1, a2, a3, b10, b11);
-            }
+        for (int m = 0; m < MT; ++m) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(v_base + pv_off + m * 32, a0, a1, a2, a3);
+            mma_bf16(o[m], a0, a1, a2, a3, b00, b01);
+            mma_bf16(o[m], a0, a1, a2, a3, b10, b11);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
