@@ -25,8 +25,9 @@
 //              K = d), P through a per-warp smem tile (bf16 hi + bf16 residual,
 //              ~16 mantissa bits), O^T += V^T P^T (M = 16 channels x d/16 tiles,
 //              N = 8 heads, K = the warp's 16 rows). No cross-warp barrier in the
-//              chunk loop. A run of chunks of one unit ends in a per-warp partial
-//              (m, l, o[G][d]); the warp that completes a unit merges its partials
+//              chunk loop. At the end of a run of chunks of one unit the 8 splits
+//              are combined in smem (deterministic tree) into one partial
+//              (m, l, o[G][d]); the CTA that completes a unit merges its partials
 //              (LSE merge fused into the kernel, deferred to the end of the range).
 //
 // Bank conflicts without TMA swizzle: a page lands contiguously in smem, so rows
@@ -86,6 +87,10 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
     return old;
 }
 
+__device__ __forceinline__ void consumer_sync() {  // named barrier 1: consumer warps only
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers) : "memory");
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
                                         uint32_t& a3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -116,16 +121,22 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
 struct StageMeta {
     __align__(16) uint16_t q[8 * 128];  // the chunk's unit's G query rows (bf16)
     uint32_t unit;
-    uint32_t chunk;
-    uint32_t any_invalid;       // some row of the chunk carries no token
-    uint16_t valid[kMaxSlots];  // valid rows per page slot (0..P)
+    uint32_t chunk;             // bit 31: some row of the chunk carries no token
+    uint8_t valid[kMaxSlots];   // valid rows per page slot (0..P; P <= 128)
 };
 
+template <int D>
 struct SmemHead {  // fixed-size part after the stage tiles
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     StageMeta meta[kStages];
-    uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
+    float ml[kWarps][8][2];  // per-warp (m, l) per head, exchanged at a flush
+    uint32_t pend[kWarps];   // units to merge at the end of the range
+    uint32_t flag;
+    union {
+        uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
+        float red[kWarps / 2][8][D / 2];      // cross-warp reduction of O (half the channels)
+    } u;
 };
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     const uint32_t NS = kRows / P;  // page slots per chunk
     const uint32_t TB = tile_bytes(D, P);
     const uint32_t slot_stride = P * D * 2 + 16;
-    SmemHead& sh = *reinterpret_cast<SmemHead*>(smem + kStages * 2 * TB);
+    SmemHead<D>& sh = *reinterpret_cast<SmemHead<D>*>(smem + kStages * 2 * TB);
     const uint32_t smem_base = smem_u32(smem);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -214,14 +225,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
                 const uint32_t s = k * 32 + lane;
-                if (s < NS) mt.valid[s] = uint16_t(vl[k]);
+                if (s < NS) mt.valid[s] = uint8_t(vl[k]);
                 bytes += __reduce_add_sync(0xffffffffu, vl[k] ? 2 * P * D * 2 : 0u);
                 invalid |= __ballot_sync(0xffffffffu, s < NS && vl[k] < P);
             }
             if (lane == 0) {
                 mt.unit = u;
-                mt.chunk = c;
-                mt.any_invalid = invalid ? 1u : 0u;
+                mt.chunk = c | (invalid ? 0x80000000u : 0u);
                 // the unit's G query rows ride along (units are b-major: the q row block
                 // of unit u = b*H + h starts at u * G * D)
                 mbar_expect_tx(full, bytes + L.G * D * 2);
@@ -268,26 +278,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         rv_slot[hh] = row & (NS - 1);
         rv_row[hh] = row >> ns_log;
     }
-    uint16_t* pt0 = sh.p[warp][0];
-    uint16_t* pt1 = sh.p[warp][1];
+    uint16_t* pt0 = sh.u.p[warp][0];
+    uint16_t* pt1 = sh.u.p[warp][1];
 
     uint32_t cur_u = 0xffffffffu, seg_first = 0, seg_last = 0;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // partial slot of (unit, first chunk of a run, warp)
-    auto slot_of = [&](uint32_t unit, uint32_t chunk, uint32_t wp) -> size_t {
-        return (size_t(unit) * slots_per_unit + chunk) * kWarps + wp;
+    // partial slot of (unit, first chunk of a run)
+    auto slot_of = [&](uint32_t unit, uint32_t chunk) -> size_t {
+        return size_t(unit) * slots_per_unit + chunk;
     };
 
     // LSE merge of all partials of unit mu into `out` by this warp (all G heads).
     // Lane-parallel over partial slots: weights exp2(m - M) are computed for 32
     // slots at a time and only slots holding a real partial (weight != 0) are read.
     auto merge = [&](uint32_t mu) {
-        const uint32_t nslots = (chunk_base[mu + 1] - chunk_base[mu]) * kWarps;
-        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16;
-        const float* pou = part_o + slot_of(mu, 0, 0) * 8 * D;
+        const uint32_t nslots = chunk_base[mu + 1] - chunk_base[mu];
+        const float* mlu = part_ml + slot_of(mu, 0) * 16;
+        const float* pou = part_o + slot_of(mu, 0) * 8 * D;
         constexpr int PER = D / 32;
         for (uint32_t h = 0; h < G; ++h) {
             float M = -INFINITY;
@@ -320,62 +330,126 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     };
 
-    // Units this warp completed: merged after the chunk loop so a merge never stalls
-    // the pipeline mid-range (a full list merges immediately).
-    constexpr int kMaxPend = 4;
-    uint32_t pend[kMaxPend];
-    int npend = 0;
+    // Units whose last partial this CTA wrote: merged after the chunk loop (warp i
+    // takes the i-th), so a merge never stalls the pipeline mid-range.
+    constexpr int kMaxPend = kWarps;
+    uint32_t npend = 0;  // CTA-uniform
 
-    // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count the
-    // chunks; the warp completing the unit schedules its merge.
+    // Emit the CTA's partial of (cur_u, chunks seg_first..seg_last). All consumer
+    // warps reach unit boundaries at the same chunk, so their 8 row splits are
+    // combined here (deterministic smem tree), and one partial per run is written.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
-        const size_t slot = slot_of(cur_u, seg_first, warp);
-        float* po = part_o + slot * 8 * D;
-        float* ml = part_ml + slot * 16;
+        if (g == 0) {
+            sh.ml[warp][2 * t4][0] = m_run[0];
+            sh.ml[warp][2 * t4][1] = lsum[0];
+            sh.ml[warp][2 * t4 + 1][0] = m_run[1];
+            sh.ml[warp][2 * t4 + 1][1] = lsum[1];
+        }
+        consumer_sync();
+        float M[2], Ltot[2];
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-            const uint32_t c0 = m * 16 + g;
+        for (int hc = 0; hc < 2; ++hc) {
+            const int h = 2 * t4 + hc;
+            M[hc] = -INFINITY;
 #pragma unroll
-            for (int hc = 0; hc < 2; ++hc) {
-                const uint32_t h = 2 * t4 + hc;
-                if (h < G) {
-                    po[h * D + c0] = o[m][hc];
-                    po[h * D + c0 + 8] = o[m][2 + hc];
-                }
+            for (int w2 = 0; w2 < kWarps; ++w2) M[hc] = fmaxf(M[hc], sh.ml[w2][h][0]);
+            Ltot[hc] = 0.0f;
+#pragma unroll
+            for (int w2 = 0; w2 < kWarps; ++w2) {
+                const float mw = sh.ml[w2][h][0];
+                Ltot[hc] += mw == -INFINITY ? 0.0f : exp2f(mw - M[hc]) * sh.ml[w2][h][1];
+            }
+            const float e = m_run[hc] == -INFINITY ? 0.0f : exp2f(m_run[hc] - M[hc]);
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                o[m][hc] *= e;
+                o[m][2 + hc] *= e;
             }
         }
-        if (g == 0) {  // m and l are warp-uniform per head
-            ml[(2 * t4) * 2] = m_run[0];
-            ml[(2 * t4) * 2 + 1] = lsum[0];
-            ml[(2 * t4 + 1) * 2] = m_run[1];
-            ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
+        // o fragments: o[m][hc] = O[ch m*16+g][head 2t4+hc], o[m][2+hc] = ch + 8
+        // tree over warps, one half of the channels (m-tiles) at a time
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh) {
+#pragma unroll
+            for (int half = kWarps / 2; half >= 1; half >>= 1) {
+                if (warp >= uint32_t(half) && warp < uint32_t(2 * half)) {
+#pragma unroll
+                    for (int m = mh * MT / 2; m < (mh + 1) * MT / 2; ++m)
+#pragma unroll
+                        for (int hc = 0; hc < 2; ++hc) {
+                            const int cl = (m - mh * MT / 2) * 16 + g;
+                            sh.u.red[warp - half][2 * t4 + hc][cl] = o[m][hc];
+                            sh.u.red[warp - half][2 * t4 + hc][cl + 8] = o[m][2 + hc];
+                        }
+                }
+                consumer_sync();
+                if (warp < uint32_t(half)) {
+#pragma unroll
+                    for (int m = mh * MT / 2; m < (mh + 1) * MT / 2; ++m)
+#pragma unroll
+                        for (int hc = 0; hc < 2; ++hc) {
+                            const int cl = (m - mh * MT / 2) * 16 + g;
+                            o[m][hc] += sh.u.red[warp][2 * t4 + hc][cl];
+                            o[m][2 + hc] += sh.u.red[warp][2 * t4 + hc][cl + 8];
+                        }
+                }
+                consumer_sync();
+            }
         }
-        // the run's other chunks carry no partial of their own (for this warp)
-        for (uint32_t c = seg_first + 1 + lane / 8; c <= seg_last; c += 4) {
-            float* mc = part_ml + slot_of(cur_u, c, warp) * 16;
-            mc[(lane % 8) * 2] = -INFINITY;
-            mc[(lane % 8) * 2 + 1] = 0.0f;
+        if (warp == 0) {
+            const size_t slot = slot_of(cur_u, seg_first);
+            float* po = part_o + slot * 8 * D;
+            float* ml = part_ml + slot * 16;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const uint32_t c0 = m * 16 + g;
+#pragma unroll
+                for (int hc = 0; hc < 2; ++hc) {
+                    const uint32_t h = 2 * t4 + hc;
+                    if (h < G) {
+                        po[h * D + c0] = o[m][hc];
+                        po[h * D + c0 + 8] = o[m][2 + hc];
+                    }
+                }
+            }
+            if (g == 0) {
+                ml[(2 * t4) * 2] = M[0];
+                ml[(2 * t4) * 2 + 1] = Ltot[0];
+                ml[(2 * t4 + 1) * 2] = M[1];
+                ml[(2 * t4 + 1) * 2 + 1] = Ltot[1];
+            }
+            // the run's other chunks carry no partial of their own
+            for (uint32_t c = seg_first + 1 + lane / 8; c <= seg_last; c += 4) {
+                float* mc = part_ml + slot_of(cur_u, c) * 16;
+                mc[(lane % 8) * 2] = -INFINITY;
+                mc[(lane % 8) * 2 + 1] = 0.0f;
+            }
+            // completion counting: the release publishes this partial to the CTA
+            // that completes the unit, whose acquire makes all partials visible
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
+                const uint32_t mine = seg_last - seg_first + 1;
+                const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
+                sh.flag = done == nch ? 1u : 0u;
+                if (done == nch) unit_done[cur_u] = 0u;  // re-arm for the next step
+            }
         }
-        // completion counting: release publishes the partials to the warp that
-        // completes the unit, whose acquire makes every partial visible to it
-        __syncwarp();
-        uint32_t last = 0;
-        if (lane == 0) {
-            const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
-            const uint32_t mine = seg_last - seg_first + 1;
-            const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
-            last = done == kWarps * nch;
-            if (last) unit_done[cur_u] = 0u;  // re-arm for the next step
+        consumer_sync();
+        if (sh.flag) {
+            if (npend == kMaxPend) {
+                if (warp == 0) merge(cur_u);
+            } else {
+                sh.pend[npend] = cur_u;
+                ++npend;
+            }
         }
-        if (__shfl_sync(0xffffffffu, last, 0)) {
-            if (npend == kMaxPend) merge(cur_u);
-            else pend[npend++] = cur_u;
-        }
+        consumer_sync();  // ml / red / flag free again
     };
 
     uint32_t stage = 0, phase = 0;
@@ -386,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         if (u != cur_u) {
             if (cur_u != 0xffffffffu) flush();
             cur_u = u;
-            seg_first = mt.chunk;
+            seg_first = mt.chunk & 0x7fffffffu;
             m_run[0] = m_run[1] = -INFINITY;
             l_run[0] = l_run[1] = 0.0f;
 #pragma unroll
@@ -399,10 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
             }
         }
-        seg_last = mt.chunk;
+        seg_last = mt.chunk & 0x7fffffffu;
         const uint32_t k_base = smem_base + stage * 2 * TB;
         const uint32_t v_base = k_base + TB;
-        const bool any_invalid = mt.any_invalid != 0;
+        const bool any_invalid = (mt.chunk >> 31) != 0;
         if (any_invalid) {
             // zero this warp's V rows that carry no token: stale or uninitialised smem
             // could hold NaN/Inf, and 0 * NaN would poison the PV product
@@ -479,13 +553,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     }
     if (cur_u != 0xffffffffu) flush();
-    for (int i = 0; i < npend; ++i) merge(pend[i]);
+    if (warp < npend) merge(sh.pend[warp]);
 }
 
 }  // namespace
 
 size_t attend_smem_bytes(uint32_t D, uint32_t P) {
-    return size_t(kStages) * 2 * tile_bytes(D, P) + sizeof(SmemHead);
+    return size_t(kStages) * 2 * tile_bytes(D, P) + (D == 64 ? sizeof(SmemHead<64>) : sizeof(SmemHead<128>));
 }
 
 cudaError_t init_attend_attributes() {
