@@ -490,19 +490,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             __syncwarp();
         }
 
-        // S^T = K Q^T over the warp's 16 rows: two accumulator chains (even / odd ks)
-        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        // Pull this warp's K and V fragments (16 rows x d) into registers, then release
+        // the stage at once: the math below runs on registers while the producer is
+        // already refilling the stage, so a stage is held only for the ldmatrix latency.
+        uint32_t kf[D / 16][4], vf[MT][4];
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-            uint32_t a0, a1, a2, a3;
-            ldsm_x4(k_base + qk_off + ks * 32, a0, a1, a2, a3);
-            mma_bf16((ks & 1) ? s2 : s, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-        }
+        for (int ks = 0; ks < D / 16; ++ks)
+            ldsm_x4(k_base + qk_off + ks * 32, kf[ks][0], kf[ks][1], kf[ks][2], kf[ks][3]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) s[i] += s2[i];
+        for (int m = 0; m < MT; ++m) ldsm_x4_t(v_base + pv_off + m * 32, vf[m][0], vf[m][1], vf[m][2], vf[m][3]);
         bool rv[2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) rv[hh] = !any_invalid || rv_row[hh] < mt.valid[rv_slot[hh]];
+        // the fragments must have left shared memory before the stage is released:
+        // an empty asm consuming every fragment register makes the warp wait for them
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+            asm volatile("" ::"r"(kf[ks][0]), "r"(kf[ks][1]), "r"(kf[ks][2]), "r"(kf[ks][3]) : "memory");
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+            asm volatile("" ::"r"(vf[m][0]), "r"(vf[m][1]), "r"(vf[m][2]), "r"(vf[m][3]) : "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
+
+        // S^T = K Q^T over the warp's 16 rows: two accumulator chains (even / odd ks)
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+            mma_bf16((ks & 1) ? s2 : s, kf[ks][0], kf[ks][1], kf[ks][2], kf[ks][3], qb[ks][0], qb[ks][1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i] += s2[i];
         // warp-local online softmax: this warp is its own split
         float mnew[2];
 #pragma unroll
@@ -538,15 +555,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         const uint32_t b01 = *reinterpret_cast<const uint32_t*>(pt0 + g * kPStride + 8 + 2 * t4);
         const uint32_t b10 = *reinterpret_cast<const uint32_t*>(pt1 + g * kPStride + 2 * t4);
         const uint32_t b11 = *reinterpret_cast<const uint32_t*>(pt1 + g * kPStride + 8 + 2 * t4);
+        __syncwarp();  // P tile reads done before the next chunk overwrites it
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
-            uint32_t a0, a1, a2, a3;
-            ldsm_x4_t(v_base + pv_off + m * 32, a0, a1, a2, a3);
-            mma_bf16(o[m], a0, a1, a2, a3, b00, b01);
-            mma_bf16(o[m], a0, a1, a2, a3, b10, b11);
+            mma_bf16(o[m], vf[m][0], vf[m][1], vf[m][2], vf[m][3], b00, b01);
+            mma_bf16(o[m], vf[m][0], vf[m][1], vf[m][2], vf[m][3], b10, b11);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
         if (++stage == kStages) {
             stage = 0;
             phase ^= 1;

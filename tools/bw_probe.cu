@@ -40,7 +40,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 constexpr int kConsumerWarps = 4;
 
 __global__ void k_bulk(const char* pool, const uint32_t* perm, uint32_t n_pages, uint32_t page, uint32_t stage,
-                       uint32_t stages, unsigned long long* sink) {
+                       uint32_t stages, unsigned long long* sink, long long hold_cycles) {
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + stages * stage);
     unsigned long long* empty = full + stages;
@@ -75,6 +75,10 @@ __global__ void k_bulk(const char* pool, const uint32_t* perm, uint32_t n_pages,
     for (uint32_t c = c0; c < c1; ++c) {
         mbar_wait(smem_u32(&full[st]), ph);
         acc += smem[st * stage + threadIdx.x * 16];
+        if (hold_cycles) {  // emulate consumer compute holding the stage
+            const long long t0 = clock64();
+            while (clock64() - t0 < hold_cycles) {}
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
         if (++st == stages) { st = 0; ph ^= 1; }
@@ -108,8 +112,9 @@ int main(int argc, char** argv) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const size_t read_bytes = size_t(1) << 30;  // bytes moved per run
     struct Cfg { uint32_t page, stage, stages; };
-    std::vector<Cfg> cfgs = {{4096, 65536, 3}, {2048, 65536, 3}, {1024, 65536, 3}, {4096, 32768, 6},
-                             {4096, 16384, 12}, {8192, 65536, 3}, {16384, 65536, 3}, {4096, 49152, 4}};
+    std::vector<Cfg> cfgs = {{4096, 65536, 3}, {4096, 32768, 6}, {4096, 49152, 4}, {4096, 16384, 12},
+                             {2048, 32768, 6}, {1024, 32768, 6}};
+    const long long holds[] = {0, 1000, 2000, 3000, 4000};  // SM cycles (~0.5 ns each)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -124,14 +129,11 @@ int main(int argc, char** argv) {
         cudaMemcpy(dperm, perm.data(), n_pages * 4, cudaMemcpyHostToDevice);
         const size_t smem = size_t(c.stages) * c.stage + 2 * c.stages * 8;
         cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        for (int mode = 0; mode < 2; ++mode) {
+        for (long long hold : holds) {
             float best = 1e30f;
-            for (int rep = 0; rep < 5; ++rep) {
+            for (int rep = 0; rep < 4; ++rep) {
                 cudaEventRecord(e0);
-                if (mode == 0)
-                    k_bulk<<<sms, (kConsumerWarps + 1) * 32, smem>>>(pool, dperm, n_pages, c.page, c.stage, c.stages, sink);
-                else
-                    k_ldg<<<sms * 4, 256>>>(pool, dperm, n_pages, c.page, sink);
+                k_bulk<<<sms, (kConsumerWarps + 1) * 32, smem>>>(pool, dperm, n_pages, c.page, c.stage, c.stages, sink, hold);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float ms;
@@ -139,8 +141,8 @@ int main(int argc, char** argv) {
                 if (rep) best = ms < best ? ms : best;
             }
             cudaError_t err = cudaGetLastError();
-            printf("%s page=%5u stage=%6u stages=%2u : %7.1f GB/s %s\n", mode ? "ldg " : "bulk", c.page, c.stage,
-                   c.stages, read_bytes / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
+            printf("bulk page=%5u stage=%6u stages=%2u hold=%5lld cyc : %7.1f GB/s %s\n", c.page, c.stage, c.stages,
+                   hold, read_bytes / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
         }
         cudaFree(dperm);
     }
