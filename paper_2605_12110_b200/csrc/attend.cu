@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
+__global__ void __maxnreg__(224) k_attn(LayerView L, const uint16_t* __restrict__ q,
                                                       PageList pages,
                                                       const uint32_t* __restrict__ chunk_unit,
                                                       const uint32_t* __restrict__ chunk_idx,
@@ -294,12 +294,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     // LSE merge of all partials of unit mu into `out` by this warp (all G heads).
     // Lane-parallel over partial slots: weights exp2(m - M) are computed for 32
     // slots at a time and only slots holding a real partial (weight != 0) are read.
-    auto merge = [&](uint32_t mu) {
+    auto merge = [&](uint32_t mu, uint32_t h_begin, uint32_t h_end) {
         const uint32_t nslots = chunk_base[mu + 1] - chunk_base[mu];
         const float* mlu = part_ml + slot_of(mu, 0) * 16;
         const float* pou = part_o + slot_of(mu, 0) * 8 * D;
         constexpr int PER = D / 32;
-        for (uint32_t h = 0; h < G; ++h) {
+        for (uint32_t h = h_begin; h < h_end; ++h) {
             float M = -INFINITY;
             for (uint32_t c = lane; c < nslots; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
 #pragma unroll
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         consumer_sync();
         if (sh.flag) {
             if (npend == kMaxPend) {
-                if (warp == 0) merge(cur_u);
+                if (warp == 0) merge(cur_u, 0, G);
             } else {
                 sh.pend[npend] = cur_u;
                 ++npend;
@@ -457,23 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         mbar_wait(smem_u32(&sh.full[stage]), phase);
         const StageMeta& mt = sh.meta[stage];
         const uint32_t u = mt.unit;
-        if (u != cur_u) {
-            if (cur_u != 0xffffffffu) flush();
-            cur_u = u;
-            seg_first = mt.chunk & 0x7fffffffu;
-            m_run[0] = m_run[1] = -INFINITY;
-            l_run[0] = l_run[1] = 0.0f;
-#pragma unroll
-            for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
-            // Q^T fragments (B operand): b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]
-            const uint16_t* qrow = mt.q + g * D;
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                qb[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
-                qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
-            }
-        }
-        seg_last = mt.chunk & 0x7fffffffu;
+        const uint32_t chunk = mt.chunk & 0x7fffffffu;
+        const bool new_unit = u != cur_u;
         const uint32_t k_base = smem_base + stage * 2 * TB;
         const uint32_t v_base = k_base + TB;
         const bool any_invalid = (mt.chunk >> 31) != 0;
@@ -490,15 +475,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             __syncwarp();
         }
 
-        // Pull this warp's K and V fragments (16 rows x d) into registers, then release
-        // the stage at once: the math below runs on registers while the producer is
-        // already refilling the stage, so a stage is held only for the ldmatrix latency.
-        uint32_t kf[D / 16][4], vf[MT][4];
+        // Pull this warp's K and V fragments (16 rows x d), and on a unit change the new
+        // Q^T fragments, into registers; then release the stage at once. The math and
+        // any flush of the previous unit run on registers while the producer is already
+        // refilling the stage, so a stage is held only for the ldmatrix latency.
+        uint32_t kf[D / 16][4], vf[MT][4], qn[D / 16][2];
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
             ldsm_x4(k_base + qk_off + ks * 32, kf[ks][0], kf[ks][1], kf[ks][2], kf[ks][3]);
 #pragma unroll
         for (int m = 0; m < MT; ++m) ldsm_x4_t(v_base + pv_off + m * 32, vf[m][0], vf[m][1], vf[m][2], vf[m][3]);
+        if (new_unit) {
+            // Q^T fragments (B operand): b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]
+            const uint16_t* qrow = mt.q + g * D;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                qn[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+                qn[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
+            }
+        }
         bool rv[2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) rv[hh] = !any_invalid || rv_row[hh] < mt.valid[rv_slot[hh]];
@@ -510,8 +505,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
         for (int m = 0; m < MT; ++m)
             asm volatile("" ::"r"(vf[m][0]), "r"(vf[m][1]), "r"(vf[m][2]), "r"(vf[m][3]) : "memory");
+        if (new_unit) {
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) asm volatile("" ::"r"(qn[ks][0]), "r"(qn[ks][1]) : "memory");
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
+
+        if (new_unit) {
+            if (cur_u != 0xffffffffu) flush();
+            cur_u = u;
+            seg_first = chunk;
+            m_run[0] = m_run[1] = -INFINITY;
+            l_run[0] = l_run[1] = 0.0f;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                qb[ks][0] = qn[ks][0];
+                qb[ks][1] = qn[ks][1];
+            }
+        }
+        seg_last = chunk;
 
         // S^T = K Q^T over the warp's 16 rows: two accumulator chains (even / odd ks)
         float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -567,7 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     }
     if (cur_u != 0xffffffffu) flush();
-    if (warp < npend) merge(sh.pend[warp]);
+    // pending merges: warp w takes (unit, head) pairs w, w + 8, ...
+    for (uint32_t j = warp; j < npend * G; j += kWarps) merge(sh.pend[j / G], j % G, j % G + 1);
 }
 
 }  // namespace
