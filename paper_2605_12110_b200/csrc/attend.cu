@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t
 }
 
 template <int D>
-__global__ void __maxnreg__(224) k_attn(LayerView L, const uint16_t* __restrict__ q,
+__global__ void __maxnreg__(200) k_attn(LayerView L, const uint16_t* __restrict__ q,
                                                       PageList pages,
                                                       const uint32_t* __restrict__ chunk_unit,
                                                       const uint32_t* __restrict__ chunk_idx,
