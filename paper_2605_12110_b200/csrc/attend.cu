@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t
 }
 
 template <int D>
-__global__ void __maxnreg__(200) k_attn(LayerView L, const uint16_t* __restrict__ q,
+__global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
                                                       PageList pages,
                                                       const uint32_t* __restrict__ chunk_unit,
                                                       const uint32_t* __restrict__ chunk_idx,
@@ -475,40 +475,42 @@ __global__ void __maxnreg__(200) k_attn(LayerView L, const uint16_t* __restrict_
             __syncwarp();
         }
 
-        // Pull this warp's K and V fragments (16 rows x d), and on a unit change the new
-        // Q^T fragments, into registers; then release the stage at once. The math and
-        // any flush of the previous unit run on registers while the producer is already
-        // refilling the stage, so a stage is held only for the ldmatrix latency.
-        uint32_t kf[D / 16][4], vf[MT][4], qn[D / 16][2];
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-            ldsm_x4(k_base + qk_off + ks * 32, kf[ks][0], kf[ks][1], kf[ks][2], kf[ks][3]);
-#pragma unroll
-        for (int m = 0; m < MT; ++m) ldsm_x4_t(v_base + pv_off + m * 32, vf[m][0], vf[m][1], vf[m][2], vf[m][3]);
+        // On a unit change the new unit's Q^T fragments (B operand) come from the q rows
+        // staged with the chunk: b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]. The old
+        // unit's flush below needs only o / m / l, so qb can be replaced right away.
         if (new_unit) {
-            // Q^T fragments (B operand): b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]
             const uint16_t* qrow = mt.q + g * D;
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
-                qn[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
-                qn[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
+                qb[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+                qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
             }
         }
+        // S^T = K Q^T over the warp's 16 rows straight from the stage (two accumulator
+        // chains, even / odd ks); then the V fragments go to registers and the stage is
+        // released: softmax, PV and any flush of the previous unit run on registers
+        // while the producer refills it, so a stage is held only for QK + ldmatrix.
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(k_base + qk_off + ks * 32, a0, a1, a2, a3);
+            mma_bf16((ks & 1) ? s2 : s, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+        }
+        uint32_t vf[MT][4];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) ldsm_x4_t(v_base + pv_off + m * 32, vf[m][0], vf[m][1], vf[m][2], vf[m][3]);
         bool rv[2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) rv[hh] = !any_invalid || rv_row[hh] < mt.valid[rv_slot[hh]];
-        // the fragments must have left shared memory before the stage is released:
-        // an empty asm consuming every fragment register makes the warp wait for them
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-            asm volatile("" ::"r"(kf[ks][0]), "r"(kf[ks][1]), "r"(kf[ks][2]), "r"(kf[ks][3]) : "memory");
+        for (int i = 0; i < 4; ++i) s[i] += s2[i];
+        // the fragments must have left shared memory before the stage is released:
+        // empty asms consuming S and every V fragment register make the warp wait
+        asm volatile("" ::"f"(s[0]), "f"(s[1]), "f"(s[2]), "f"(s[3]) : "memory");
 #pragma unroll
         for (int m = 0; m < MT; ++m)
             asm volatile("" ::"r"(vf[m][0]), "r"(vf[m][1]), "r"(vf[m][2]), "r"(vf[m][3]) : "memory");
-        if (new_unit) {
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) asm volatile("" ::"r"(qn[ks][0]), "r"(qn[ks][1]) : "memory");
-        }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
 
@@ -520,21 +522,9 @@ __global__ void __maxnreg__(200) k_attn(LayerView L, const uint16_t* __restrict_
             l_run[0] = l_run[1] = 0.0f;
 #pragma unroll
             for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                qb[ks][0] = qn[ks][0];
-                qb[ks][1] = qn[ks][1];
-            }
         }
         seg_last = chunk;
 
-        // S^T = K Q^T over the warp's 16 rows: two accumulator chains (even / odd ks)
-        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-            mma_bf16((ks & 1) ? s2 : s, kf[ks][0], kf[ks][1], kf[ks][2], kf[ks][3], qb[ks][0], qb[ks][1]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) s[i] += s2[i];
         // warp-local online softmax: this warp is its own split
         float mnew[2];
 #pragma unroll
