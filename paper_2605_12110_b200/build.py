@@ -38,28 +38,32 @@ def _newest_input() -> float:
     return max(f.stat().st_mtime for f in files if f.is_file())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if LIB.exists() and not force and LIB.stat().st_mtime >= _newest_input():
-        return LIB
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """trace=True builds lib/libabsp_trace.so with the attention timeline
+    instrumentation (-DABSP_ATTN_TRACE, tools/attn_trace.py); never the product."""
+    lib = LIBDIR / "libabsp_trace.so" if trace else LIB
+    objdir = OBJDIR.parent / "obj_trace" if trace else OBJDIR
+    if lib.exists() and not force and lib.stat().st_mtime >= _newest_input():
+        return lib
+    objdir.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = OBJDIR / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC), "-c",
-               str(CSRC / src), "-o", str(obj)]
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, *(["-DABSP_ATTN_TRACE"] if trace else []), "-I", str(ROOT / "include"),
+               "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

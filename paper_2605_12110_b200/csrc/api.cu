@@ -717,3 +717,15 @@ absp_status absp_fill_synthetic_bf16(void* dst, uint64_t count, uint64_t seed, u
 uint64_t absp_launch_count(absp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 }  // extern "C"
+
+#ifdef ABSP_ATTN_TRACE
+// Debug builds only (not part of include/absp.h): copy the attention timeline
+// stamps (uint64 globaltimer ns, [160 CTAs][256 slots]) to host memory.
+namespace absp {
+cudaError_t debug_attn_trace(void* dst, size_t bytes);
+}
+extern "C" absp_status absp_debug_attn_trace(void* dst, size_t bytes) {
+    cudaError_t e = absp::debug_attn_trace(dst, bytes);
+    return e == cudaSuccess ? ABSP_OK : cuda_fail(e, "debug_attn_trace");
+}
+#endif

@@ -52,6 +52,23 @@ constexpr int kWarpRows = kRows / kWarps;  // 16
 constexpr int kPStride = kWarpRows + 8;    // bf16 row stride of a P tile (bank-conflict free)
 constexpr int kMaxSlots = kRows;           // P >= 1
 
+// Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
+// globaltimer stamps of the producer's issues, warp 0's data arrivals / releases,
+// flushes and merges. Read back with absp_debug_attn_trace.
+#ifdef ABSP_ATTN_TRACE
+constexpr int kTraceSlots = 256;
+__device__ unsigned long long g_attn_trace[160 * kTraceSlots];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define ATTN_TRACE(slot) \
+    do { if (blockIdx.x < 160 && (slot) < kTraceSlots) g_attn_trace[blockIdx.x * kTraceSlots + (slot)] = gtime(); } while (0)
+#else
+#define ATTN_TRACE(slot) do {} while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -179,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    if (tid == 0) ATTN_TRACE(0);
     __syncthreads();
 
     if (warp == kWarps) {
@@ -247,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                     bulk_g2s(kdst + TB + s * slot_stride, L.v_pool + off, P * D * 2, full);
                 }
             }
+            if (lane == 0) ATTN_TRACE(1 + (w - w_begin));  // producer issued chunk
             if (++stage == kStages) {
                 stage = 0;
                 phase ^= 1;
@@ -452,9 +471,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         consumer_sync();  // ml / red / flag free again
     };
 
-    uint32_t stage = 0, phase = 0;
+    uint32_t stage = 0, phase = 0, nflush = 0;
+    (void)nflush;
     for (uint32_t w = w_begin; w < w_end; ++w) {
         mbar_wait(smem_u32(&sh.full[stage]), phase);
+        if (tid == 0) ATTN_TRACE(64 + (w - w_begin));  // data arrived (warp 0)
         const StageMeta& mt = sh.meta[stage];
         const uint32_t u = mt.unit;
         const uint32_t chunk = mt.chunk & 0x7fffffffu;
@@ -513,9 +534,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             asm volatile("" ::"r"(vf[m][0]), "r"(vf[m][1]), "r"(vf[m][2]), "r"(vf[m][3]) : "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
+        if (tid == 0) ATTN_TRACE(128 + (w - w_begin));  // stage released (warp 0)
 
         if (new_unit) {
+            if (tid == 0) ATTN_TRACE(192 + 2 * (nflush & 3));
             if (cur_u != 0xffffffffu) flush();
+            if (tid == 0) ATTN_TRACE(193 + 2 * (nflush & 3));
+            ++nflush;
             cur_u = u;
             seg_first = chunk;
             m_run[0] = m_run[1] = -INFINITY;
@@ -571,12 +596,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             phase ^= 1;
         }
     }
+    if (tid == 0) ATTN_TRACE(240);
     if (cur_u != 0xffffffffu) flush();
+    if (tid == 0) ATTN_TRACE(241);
     // pending merges: warp w takes (unit, head) pairs w, w + 8, ...
     for (uint32_t j = warp; j < npend * G; j += kWarps) merge(sh.pend[j / G], j % G, j % G + 1);
+    if (lane == 0) ATTN_TRACE(242 + warp);  // per-warp end (merges done)
 }
 
 }  // namespace
+
+#ifdef ABSP_ATTN_TRACE
+cudaError_t debug_attn_trace(void* dst, size_t bytes) {
+    return cudaMemcpyFromSymbol(dst, g_attn_trace, bytes);
+}
+#endif
 
 size_t attend_smem_bytes(uint32_t D, uint32_t P) {
     return size_t(kStages) * 2 * tile_bytes(D, P) + (D == 64 ? sizeof(SmemHead<64>) : sizeof(SmemHead<128>));
