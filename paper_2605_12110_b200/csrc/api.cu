@@ -219,8 +219,9 @@ absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t c
     ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
     ABSP_CUDA(cudaMemset(wl.valid.p, 0, n_slots * 2));
-    ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(slots) * 8 * D));  // one partial per CTA run
-    ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(slots) * 16));
+    // one partial slot per (chunk, consumer warp)
+    ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(slots) * kAttnSplits * 8 * D));
+    ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(slots) * kAttnSplits * 16));
     return ABSP_OK;
 }
 

@@ -24,11 +24,13 @@
 //              mma.m16n8k16 (M = 16 KV rows, N = 8 query heads of the GQA group,
 //              K = d), P through a per-warp smem tile (bf16 hi + bf16 residual,
 //              ~16 mantissa bits), O^T += V^T P^T (M = 16 channels x d/16 tiles,
-//              N = 8 heads, K = the warp's 16 rows). No cross-warp barrier in the
-//              chunk loop. At the end of a run of chunks of one unit the 8 splits
-//              are combined in smem (deterministic tree) into one partial
-//              (m, l, o[G][d]); the CTA that completes a unit merges its partials
-//              (LSE merge fused into the kernel, deferred to the end of the range).
+//              N = 8 heads, K = the warp's 16 rows). A warp takes its fragments
+//              into registers and releases the stage before the softmax/PV math, so
+//              a stage is held only for QK + ldmatrix. No cross-warp barrier: at the
+//              end of a run of chunks of one unit each warp writes its own partial
+//              (m, l, o[G][d]) and counts its chunks; the warp completing a unit
+//              queues its LSE merge, done by the CTA's warps after the chunk loop
+//              (one warp per (unit, head), loads issued in bulk).
 //
 // Bank conflicts without TMA swizzle: a page lands contiguously in smem, so rows
 // of one page are 256 B apart (same banks). Page slots are staggered by 16 B and
@@ -51,6 +53,7 @@ constexpr int kStages = 3;
 constexpr int kWarpRows = kRows / kWarps;  // 16
 constexpr int kPStride = kWarpRows + 8;    // bf16 row stride of a P tile (bank-conflict free)
 constexpr int kMaxSlots = kRows;           // P >= 1
+constexpr int kMaxPend = 32;               // units completed by one CTA
 
 // Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
 // globaltimer stamps of the producer's issues, warp 0's data arrivals / releases,
@@ -147,13 +150,9 @@ struct SmemHead {  // fixed-size part after the stage tiles
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     StageMeta meta[kStages];
-    float ml[kWarps][8][2];  // per-warp (m, l) per head, exchanged at a flush
-    uint32_t pend[kWarps];   // units to merge at the end of the range
-    uint32_t flag;
-    union {
-        uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
-        float red[kWarps / 2][8][D / 2];      // cross-warp reduction of O (half the channels)
-    } u;
+    uint32_t npend;          // units this CTA completed (merged after the chunk loop)
+    uint32_t pend[kMaxPend];
+    uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
 };
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
@@ -190,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     const uint32_t w_end = range_begin(blockIdx.x + 1, n_work, gridDim.x);
 
     if (tid == 0) {
+        sh.npend = 0u;
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&sh.full[s]), 1);
             mbar_init(smem_u32(&sh.empty[s]), kWarps);  // every consumer warp
@@ -297,178 +297,143 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         rv_slot[hh] = row & (NS - 1);
         rv_row[hh] = row >> ns_log;
     }
-    uint16_t* pt0 = sh.u.p[warp][0];
-    uint16_t* pt1 = sh.u.p[warp][1];
+    uint16_t* pt0 = sh.p[warp][0];
+    uint16_t* pt1 = sh.p[warp][1];
 
     uint32_t cur_u = 0xffffffffu, seg_first = 0, seg_last = 0;
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // partial slot of (unit, first chunk of a run)
-    auto slot_of = [&](uint32_t unit, uint32_t chunk) -> size_t {
-        return size_t(unit) * slots_per_unit + chunk;
+    // partial slot of (unit, first chunk of a run, warp)
+    auto slot_of = [&](uint32_t unit, uint32_t chunk, uint32_t wp) -> size_t {
+        return (size_t(unit) * slots_per_unit + chunk) * kWarps + wp;
     };
 
-    // LSE merge of all partials of unit mu into `out` by this warp (all G heads).
-    // Lane-parallel over partial slots: weights exp2(m - M) are computed for 32
-    // slots at a time and only slots holding a real partial (weight != 0) are read.
-    auto merge = [&](uint32_t mu, uint32_t h_begin, uint32_t h_end) {
-        const uint32_t nslots = chunk_base[mu + 1] - chunk_base[mu];
-        const float* mlu = part_ml + slot_of(mu, 0) * 16;
-        const float* pou = part_o + slot_of(mu, 0) * 8 * D;
+    // LSE merge of every partial of unit mu for query head h into `out` (one warp).
+    // Loads are issued in bulk: the (m, l) of all slots (lanes stride the slots),
+    // then the o rows of the live slots four at a time.
+    auto merge = [&](uint32_t mu, uint32_t h) {
         constexpr int PER = D / 32;
-        for (uint32_t h = h_begin; h < h_end; ++h) {
-            float M = -INFINITY;
-            for (uint32_t c = lane; c < nslots; c += 32) M = fmaxf(M, __ldcg(mlu + c * 16 + h * 2));
+        constexpr int MAXW = 8;  // 32-slot windows held in registers (<= 256 slots)
+        const uint32_t nslots = (chunk_base[mu + 1] - chunk_base[mu]) * kWarps;
+        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16;
+        const float* pou = part_o + slot_of(mu, 0, 0) * 8 * D;
+        float acc[PER];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-            float acc[PER];
+        for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
+        float lsum = 0.0f, M = -INFINITY;
+        for (uint32_t base = 0; base < nslots; base += 32 * MAXW) {
+            float mv[MAXW], lv[MAXW];
 #pragma unroll
-            for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
-            float lsum = 0.0f;
-            for (uint32_t c0 = 0; c0 < nslots; c0 += 32) {
-                const uint32_t c = c0 + lane;
-                const float m = c < nslots ? __ldcg(mlu + c * 16 + h * 2) : -INFINITY;
-                const float wgt = m == -INFINITY ? 0.0f : exp2f(m - M);
-                lsum += wgt == 0.0f ? 0.0f : wgt * __ldcg(mlu + c * 16 + h * 2 + 1);
-                for (uint32_t live = __ballot_sync(0xffffffffu, wgt != 0.0f); live; live &= live - 1) {
-                    const uint32_t src = __ffs(live) - 1;
-                    const float wc = __shfl_sync(0xffffffffu, wgt, src);
-                    const float* pc = pou + ((c0 + src) * 8 + h) * D;
+            for (int k = 0; k < MAXW; ++k) {
+                const uint32_t c = base + k * 32 + lane;
+                mv[k] = c < nslots ? __ldcg(mlu + c * 16 + h * 2) : -INFINITY;
+                lv[k] = c < nslots ? __ldcg(mlu + c * 16 + h * 2 + 1) : 0.0f;
+            }
+            float Mw = -INFINITY;
 #pragma unroll
-                    for (int i = 0; i < PER; ++i) acc[i] += wc * __ldcg(pc + lane + 32 * i);
+            for (int k = 0; k < MAXW; ++k) Mw = fmaxf(Mw, mv[k]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, off));
+            if (Mw == -INFINITY) continue;
+            // rescale what was accumulated from earlier windows
+            const float Mn = fmaxf(M, Mw);
+            const float r = M == -INFINITY ? 0.0f : exp2f(M - Mn);
+            lsum *= r;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) acc[i] *= r;
+            M = Mn;
+#pragma unroll
+            for (int k = 0; k < MAXW; ++k) {
+                const float wgt = mv[k] == -INFINITY ? 0.0f : exp2f(mv[k] - M);
+                lsum += wgt * lv[k];
+                uint32_t live = __ballot_sync(0xffffffffu, wgt != 0.0f);
+                while (live) {
+                    uint32_t src[4];
+                    float wc[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        src[j] = live ? __ffs(live) - 1 : 32u;
+                        live = live ? live & (live - 1) : 0u;
+                        wc[j] = __shfl_sync(0xffffffffu, wgt, src[j] & 31);
+                        if (src[j] == 32u) wc[j] = 0.0f;
+                    }
+                    float v[4][PER];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float* pc = pou + ((base + k * 32 + (src[j] & 31)) * 8 + h) * D;
+#pragma unroll
+                        for (int i = 0; i < PER; ++i) v[j][i] = src[j] == 32u ? 0.0f : __ldcg(pc + lane + 32 * i);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int i = 0; i < PER; ++i) acc[i] += wc[j] * v[j][i];
                 }
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
-            const float inv = 1.0f / lsum;
-            float* dst = out + (size_t(mu) * G + h) * D;  // out is [b][h*G + g][d], u = b*H + h
-#pragma unroll
-            for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
         }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+        const float inv = 1.0f / lsum;
+        float* dst = out + (size_t(mu) * G + h) * D;  // out is [b][h*G + g][d], u = b*H + h
+#pragma unroll
+        for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
     };
 
-    // Units whose last partial this CTA wrote: merged after the chunk loop (warp i
-    // takes the i-th), so a merge never stalls the pipeline mid-range.
-    constexpr int kMaxPend = kWarps;
-    uint32_t npend = 0;  // CTA-uniform
-
-    // Emit the CTA's partial of (cur_u, chunks seg_first..seg_last). All consumer
-    // warps reach unit boundaries at the same chunk, so their 8 row splits are
-    // combined here (deterministic smem tree), and one partial per run is written.
+    // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count its
+    // chunks; no barrier with the other warps. The warp completing a unit queues its
+    // merge, done by the CTA's warps after the chunk loop.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
-        if (g == 0) {
-            sh.ml[warp][2 * t4][0] = m_run[0];
-            sh.ml[warp][2 * t4][1] = lsum[0];
-            sh.ml[warp][2 * t4 + 1][0] = m_run[1];
-            sh.ml[warp][2 * t4 + 1][1] = lsum[1];
-        }
-        consumer_sync();
-        float M[2], Ltot[2];
+        const size_t slot = slot_of(cur_u, seg_first, warp);
+        float* po = part_o + slot * 8 * D;
+        float* ml = part_ml + slot * 16;
 #pragma unroll
-        for (int hc = 0; hc < 2; ++hc) {
-            const int h = 2 * t4 + hc;
-            M[hc] = -INFINITY;
+        for (int m = 0; m < MT; ++m) {
+            const uint32_t c0 = m * 16 + g;
 #pragma unroll
-            for (int w2 = 0; w2 < kWarps; ++w2) M[hc] = fmaxf(M[hc], sh.ml[w2][h][0]);
-            Ltot[hc] = 0.0f;
-#pragma unroll
-            for (int w2 = 0; w2 < kWarps; ++w2) {
-                const float mw = sh.ml[w2][h][0];
-                Ltot[hc] += mw == -INFINITY ? 0.0f : exp2f(mw - M[hc]) * sh.ml[w2][h][1];
-            }
-            const float e = m_run[hc] == -INFINITY ? 0.0f : exp2f(m_run[hc] - M[hc]);
-#pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                o[m][hc] *= e;
-                o[m][2 + hc] *= e;
-            }
-        }
-        // o fragments: o[m][hc] = O[ch m*16+g][head 2t4+hc], o[m][2+hc] = ch + 8
-        // tree over warps, one half of the channels (m-tiles) at a time
-#pragma unroll
-        for (int mh = 0; mh < 2; ++mh) {
-#pragma unroll
-            for (int half = kWarps / 2; half >= 1; half >>= 1) {
-                if (warp >= uint32_t(half) && warp < uint32_t(2 * half)) {
-#pragma unroll
-                    for (int m = mh * MT / 2; m < (mh + 1) * MT / 2; ++m)
-#pragma unroll
-                        for (int hc = 0; hc < 2; ++hc) {
-                            const int cl = (m - mh * MT / 2) * 16 + g;
-                            sh.u.red[warp - half][2 * t4 + hc][cl] = o[m][hc];
-                            sh.u.red[warp - half][2 * t4 + hc][cl + 8] = o[m][2 + hc];
-                        }
-                }
-                consumer_sync();
-                if (warp < uint32_t(half)) {
-#pragma unroll
-                    for (int m = mh * MT / 2; m < (mh + 1) * MT / 2; ++m)
-#pragma unroll
-                        for (int hc = 0; hc < 2; ++hc) {
-                            const int cl = (m - mh * MT / 2) * 16 + g;
-                            o[m][hc] += sh.u.red[warp][2 * t4 + hc][cl];
-                            o[m][2 + hc] += sh.u.red[warp][2 * t4 + hc][cl + 8];
-                        }
-                }
-                consumer_sync();
-            }
-        }
-        if (warp == 0) {
-            const size_t slot = slot_of(cur_u, seg_first);
-            float* po = part_o + slot * 8 * D;
-            float* ml = part_ml + slot * 16;
-#pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                const uint32_t c0 = m * 16 + g;
-#pragma unroll
-                for (int hc = 0; hc < 2; ++hc) {
-                    const uint32_t h = 2 * t4 + hc;
-                    if (h < G) {
-                        po[h * D + c0] = o[m][hc];
-                        po[h * D + c0 + 8] = o[m][2 + hc];
-                    }
+            for (int hc = 0; hc < 2; ++hc) {
+                const uint32_t h = 2 * t4 + hc;
+                if (h < G) {
+                    po[h * D + c0] = o[m][hc];
+                    po[h * D + c0 + 8] = o[m][2 + hc];
                 }
             }
-            if (g == 0) {
-                ml[(2 * t4) * 2] = M[0];
-                ml[(2 * t4) * 2 + 1] = Ltot[0];
-                ml[(2 * t4 + 1) * 2] = M[1];
-                ml[(2 * t4 + 1) * 2 + 1] = Ltot[1];
-            }
-            // the run's other chunks carry no partial of their own
-            for (uint32_t c = seg_first + 1 + lane / 8; c <= seg_last; c += 4) {
-                float* mc = part_ml + slot_of(cur_u, c) * 16;
-                mc[(lane % 8) * 2] = -INFINITY;
-                mc[(lane % 8) * 2 + 1] = 0.0f;
-            }
-            // completion counting: the release publishes this partial to the CTA
-            // that completes the unit, whose acquire makes all partials visible
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
-                const uint32_t mine = seg_last - seg_first + 1;
-                const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
-                sh.flag = done == nch ? 1u : 0u;
-                if (done == nch) unit_done[cur_u] = 0u;  // re-arm for the next step
+        }
+        if (g == 0) {  // m and l are warp-uniform per head
+            ml[(2 * t4) * 2] = m_run[0];
+            ml[(2 * t4) * 2 + 1] = lsum[0];
+            ml[(2 * t4 + 1) * 2] = m_run[1];
+            ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
+        }
+        // the run's other chunks carry no partial of their own (for this warp)
+        for (uint32_t c = seg_first + 1 + lane / 8; c <= seg_last; c += 4) {
+            float* mc = part_ml + slot_of(cur_u, c, warp) * 16;
+            mc[(lane % 8) * 2] = -INFINITY;
+            mc[(lane % 8) * 2 + 1] = 0.0f;
+        }
+        // completion counting: the release publishes this warp's partials to the warp
+        // that completes the unit, whose acquire makes every partial visible to it
+        __syncwarp();
+        uint32_t merge_now = 0;
+        if (lane == 0) {
+            const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
+            const uint32_t mine = seg_last - seg_first + 1;
+            const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
+            if (done == kWarps * nch) {
+                unit_done[cur_u] = 0u;  // re-arm for the next step
+                const uint32_t slot_p = atomicAdd(&sh.npend, 1u);
+                if (slot_p < uint32_t(kMaxPend)) sh.pend[slot_p] = cur_u;
+                else merge_now = 1u;  // queue full: this warp merges right away
             }
         }
-        consumer_sync();
-        if (sh.flag) {
-            if (npend == kMaxPend) {
-                if (warp == 0) merge(cur_u, 0, G);
-            } else {
-                sh.pend[npend] = cur_u;
-                ++npend;
-            }
-        }
-        consumer_sync();  // ml / red / flag free again
+        if (__shfl_sync(0xffffffffu, merge_now, 0))
+            for (uint32_t h = 0; h < G; ++h) merge(cur_u, h);
     };
 
     uint32_t stage = 0, phase = 0, nflush = 0;
@@ -599,8 +564,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     if (tid == 0) ATTN_TRACE(240);
     if (cur_u != 0xffffffffu) flush();
     if (tid == 0) ATTN_TRACE(241);
+    consumer_sync();
     // pending merges: warp w takes (unit, head) pairs w, w + 8, ...
-    for (uint32_t j = warp; j < npend * G; j += kWarps) merge(sh.pend[j / G], j % G, j % G + 1);
+    const uint32_t npend = min(sh.npend, uint32_t(kMaxPend));
+    for (uint32_t j = warp; j < npend * G; j += kWarps) merge(sh.pend[j / G], j % G);
     if (lane == 0) ATTN_TRACE(242 + warp);  // per-warp end (merges done)
 }
 

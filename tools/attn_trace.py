@@ -73,3 +73,26 @@ print(f"issue -> data arrival (us)             {pct(leads)}")
 print(f"flush duration (us)                    {pct(flushes)}")
 print(f"final flush + merges (us)              {pct(tails)}")
 print(f"CTA end (us)                           {pct(ends)}")
+
+# ---- in-step timeline: flush L2, then a full decode step (top-k -> attention) ----
+flush.fill_(2)
+torch.cuda.synchronize()
+da.decode_step(0, q, out)
+torch.cuda.synchronize()
+_abi.check(_abi._lib.absp_debug_attn_trace(tr.ctypes.data, tr.nbytes))
+t0 = min(int(x) for x in tr[:148, 0] if x)
+firsts, gaps, ends, tails = [], [], [], []
+for c in range(148):
+    row = tr[c]
+    arr = [rel(row[64 + i]) for i in range(64) if row[64 + i]]
+    if arr:
+        firsts.append(arr[0] - rel(row[0]))
+        gaps += list(np.diff(arr))
+    ends.append(max(rel(x) for x in row[242:250] if x))
+    if row[240]:
+        tails.append(ends[-1] - rel(row[240]))
+print("--- inside decode_step (page lists hot in L2) ---")
+print(f"kernel span                            {max(ends):.2f} us")
+print(f"first data after CTA start (us)        {pct(firsts)}")
+print(f"chunk inter-arrival at warp 0 (us)     {pct(gaps)}")
+print(f"final flush + merges (us)              {pct(tails)}")
