@@ -1,0 +1,340 @@
+/*
+ * absp.hpp — header-only C++ host layer over the C ABI (absp.h), in the shape of
+ * the reference's namespace absparse (/root/reference/proj/include/absparse):
+ *
+ *   absp::QuantSpec, CentroidMethod, QuantMode   <- config.hpp:11-26
+ *   absp::EngineConfig (+ GQA/batch/capacity)     <- config.hpp:36-52
+ *   absp::BlockAssignment, build_offsets          <- centroids.hpp:12-26
+ *   absp::StoreSnapshot (one sequence's device     <- CentroidStore + QuantizedCentroidStore
+ *     store read back in the reference layouts)      centroids.hpp:31-52, quantizer.hpp:18-38
+ *   BlockAssignment::load / save                   <- read/write_assignment_file
+ *                                                     calibrator.cpp:277-311
+ *   absp::DecodeAttention                         <- the device replacement of
+ *     build_store   = compute_block_centroids + quantize_store (centroids.hpp:56-57,
+ *                                                              quantizer.hpp:43)
+ *     select        = estimate_scores + select_topk             (engine.hpp:47-68)
+ *     attend        = populate_page_spans + sparse_attention     (engine.hpp:71-82)
+ *     decode_step   = DecodeEngine::step's estimate->select->attend (engine.cpp:450-461)
+ *
+ * Errors are rethrown as the reference's exception classes:
+ *   ABSP_EINVAL -> std::invalid_argument, ABSP_ERANGE -> std::out_of_range,
+ *   ABSP_ECAPACITY -> std::runtime_error, ABSP_ESTATE -> std::logic_error,
+ *   ABSP_ECUDA / ABSP_ENOMEM -> absp::cuda_error (a std::runtime_error).
+ *
+ * No CUDA headers are needed: device buffers are plain pointers owned by the
+ * caller (streams are cudaStream_t passed as void*). Link with -labsp.
+ */
+#ifndef ABSP_HPP
+#define ABSP_HPP
+
+#include <cstddef>
+#include <cstdint>
+#include <fstream>
+#include <optional>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "absp.h"
+
+namespace absp {
+
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// Maps a status onto the reference's exception classes.
+inline void check(absp_status st) {
+    if (st == ABSP_OK) return;
+    const std::string msg = absp_last_error();
+    switch (st) {
+        case ABSP_EINVAL: throw std::invalid_argument(msg);
+        case ABSP_ERANGE: throw std::out_of_range(msg);
+        case ABSP_ECAPACITY: throw std::runtime_error(msg);
+        case ABSP_ESTATE: throw std::logic_error(msg);
+        default: throw cuda_error(msg);
+    }
+}
+
+enum class CentroidMethod { kMean = ABSP_CENTROID_MEAN, kMaxMin = ABSP_CENTROID_MAXMIN };
+enum class QuantMode { kSymmetric = ABSP_QUANT_SYM, kAsymmetric = ABSP_QUANT_ASYM };
+
+// QuantSpec (config.hpp:17-26).
+struct QuantSpec {
+    int bits = 4;
+    QuantMode mode = QuantMode::kAsymmetric;
+    int levels() const { return (1 << bits) - 1; }
+    int sym_mid() const { return (1 << (bits - 1)) - 1; }
+    bool operator==(const QuantSpec& o) const { return bits == o.bits && mode == o.mode; }
+    void validate() const {  // config.cpp:8-12
+        if (bits != 2 && bits != 4 && bits != 8)
+            throw std::invalid_argument("quant bits must be one of {2, 4, 8}");
+    }
+};
+
+// quant_spec_name / parse_quant_spec (config.cpp:14-28).
+inline std::string quant_spec_name(const QuantSpec& s) {
+    return "int" + std::to_string(s.bits) + (s.mode == QuantMode::kSymmetric ? "xsym" : "xasym");
+}
+inline QuantSpec parse_quant_spec(const std::string& name) {
+    for (int bits : {2, 4, 8})
+        for (QuantMode m : {QuantMode::kSymmetric, QuantMode::kAsymmetric}) {
+            QuantSpec s{bits, m};
+            if (quant_spec_name(s) == name) return s;
+        }
+    throw std::invalid_argument("unknown quant spec '" + name + "'");
+}
+
+// EngineConfig (config.hpp:36-52) plus the batch / GQA / capacity extensions.
+struct EngineConfig {
+    std::size_t num_heads = 8;  // KV heads
+    std::size_t head_dim = 64;
+    std::size_t page_size = 16;
+    std::vector<std::size_t> candidate_block_sizes = {16, 32, 64};
+    std::size_t token_budget = 4096;
+    double recall_threshold = 0.98;
+    CentroidMethod centroid_method = CentroidMethod::kMean;
+    std::optional<QuantSpec> quant;
+    // extensions
+    std::size_t num_q_heads = 0;  // 0 = num_heads (MHA)
+    std::size_t max_batch = 1;
+    std::size_t max_seq_len = 131072;
+    std::size_t num_layers = 1;
+
+    std::size_t min_candidate() const {
+        std::size_t m = candidate_block_sizes.empty() ? 0 : candidate_block_sizes.front();
+        for (std::size_t b : candidate_block_sizes) m = b < m ? b : m;
+        return m;
+    }
+    std::size_t max_candidate() const {
+        std::size_t m = 0;
+        for (std::size_t b : candidate_block_sizes) m = b > m ? b : m;
+        return m;
+    }
+    std::size_t group_size() const { return (num_q_heads ? num_q_heads : num_heads) / num_heads; }
+
+    absp_config to_abi() const {
+        if (candidate_block_sizes.size() > ABSP_MAX_CANDIDATES)
+            throw std::invalid_argument("too many candidate block sizes");
+        absp_config c{};
+        c.num_kv_heads = uint32_t(num_heads);
+        c.num_q_heads = uint32_t(num_q_heads ? num_q_heads : num_heads);
+        c.head_dim = uint32_t(head_dim);
+        c.page_size = uint32_t(page_size);
+        c.num_candidates = uint32_t(candidate_block_sizes.size());
+        for (std::size_t i = 0; i < candidate_block_sizes.size(); ++i)
+            c.candidate_block_sizes[i] = uint32_t(candidate_block_sizes[i]);
+        c.token_budget = uint32_t(token_budget);
+        c.centroid_method = uint32_t(centroid_method);
+        c.quant_bits = quant ? uint32_t(quant->bits) : 0u;
+        c.quant_mode = uint32_t(quant ? quant->mode : QuantMode::kAsymmetric);
+        c.max_batch = uint32_t(max_batch);
+        c.max_seq_len = uint32_t(max_seq_len);
+        c.num_layers = uint32_t(num_layers);
+        return c;
+    }
+    // EngineConfig::validate (config.cpp:48-78) + this build's limits.
+    void validate() const {
+        if (recall_threshold <= 0.0) throw std::invalid_argument("recall_threshold must be positive");
+        if (quant) quant->validate();
+        const absp_config c = to_abi();
+        check(absp_config_validate(&c));
+    }
+};
+
+// BlockAssignment (centroids.hpp:12-23).
+struct BlockAssignment {
+    std::vector<std::size_t> block_sizes;
+
+    static BlockAssignment uniform(std::size_t num_heads, std::size_t block_size) {
+        return BlockAssignment{std::vector<std::size_t>(num_heads, block_size)};
+    }
+    // Heads cycle through the candidates (cmd_bench, cli_commands.cpp:445-451).
+    static BlockAssignment cycled(std::size_t num_heads, const std::vector<std::size_t>& cands) {
+        BlockAssignment a;
+        for (std::size_t h = 0; h < num_heads; ++h) a.block_sizes.push_back(cands[h % cands.size()]);
+        return a;
+    }
+    // read_assignment_file (calibrator.cpp:285-311): "head block_size" per line,
+    // consecutive heads from 0, empty lines skipped; std::runtime_error otherwise.
+    static BlockAssignment load(const std::string& path) {
+        std::ifstream in(path);
+        if (!in) throw std::runtime_error("read_assignment_file: cannot open " + path);
+        BlockAssignment a;
+        std::string line;
+        std::size_t expected = 0;
+        while (std::getline(in, line)) {
+            if (line.empty()) continue;
+            std::istringstream row(line);
+            std::size_t head = 0, block = 0;
+            if (!(row >> head >> block) || head != expected)
+                throw std::runtime_error("read_assignment_file: malformed line '" + line +
+                                         "' (expected 'head block_size' with consecutive heads)");
+            std::string extra;
+            if (row >> extra)
+                throw std::runtime_error("read_assignment_file: trailing tokens on line '" + line + "'");
+            a.block_sizes.push_back(block);
+            ++expected;
+        }
+        if (a.block_sizes.empty()) throw std::runtime_error("read_assignment_file: empty file " + path);
+        return a;
+    }
+    // write_assignment_file (calibrator.cpp:277-283).
+    void save(const std::string& path) const {
+        std::ofstream out(path, std::ios::trunc);
+        if (!out) throw std::runtime_error("write_assignment_file: cannot open " + path);
+        for (std::size_t h = 0; h < block_sizes.size(); ++h) out << h << ' ' << block_sizes[h] << '\n';
+    }
+    std::size_t num_heads() const { return block_sizes.size(); }
+    double average_block_size() const {
+        if (block_sizes.empty()) return 0.0;
+        double s = 0.0;
+        for (std::size_t b : block_sizes) s += double(b);
+        return s / double(block_sizes.size());
+    }
+    // BlockAssignment::validate (centroids.cpp:59-76).
+    void validate(const EngineConfig& config) const {
+        if (block_sizes.size() != config.num_heads)
+            throw std::invalid_argument("assignment covers " + std::to_string(block_sizes.size()) +
+                                        " heads, config has " + std::to_string(config.num_heads));
+        for (std::size_t h = 0; h < block_sizes.size(); ++h) {
+            const std::size_t b = block_sizes[h];
+            bool cand = false;
+            for (std::size_t c : config.candidate_block_sizes) cand |= c == b;
+            if (!cand)
+                throw std::invalid_argument("head " + std::to_string(h) + ": block size " +
+                                            std::to_string(b) + " is not a candidate");
+            if (b % config.page_size != 0)
+                throw std::invalid_argument("head " + std::to_string(h) + ": block size " +
+                                            std::to_string(b) + " is not a multiple of page_size");
+        }
+    }
+};
+
+// build_offsets (centroids.cpp:78-84).
+inline std::vector<std::size_t> build_offsets(std::size_t seq_len, const BlockAssignment& a) {
+    std::vector<std::size_t> off(a.num_heads() + 1, 0);
+    for (std::size_t h = 0; h < a.num_heads(); ++h)
+        off[h + 1] = off[h] + (seq_len + a.block_sizes[h] - 1) / a.block_sizes[h];
+    return off;
+}
+
+// One sequence's device store read back in the reference layouts
+// (CentroidStore + QuantizedCentroidStore fields, centroids.hpp:31-52,
+// quantizer.hpp:18-38; codes one per byte).
+struct StoreSnapshot {
+    std::vector<std::size_t> offsets;
+    std::vector<float> values, values_min;
+    std::vector<uint8_t> codes, codes_min;
+    std::vector<float> scales, zero_points, scales_min, zero_points_min;
+    std::size_t total_centroids() const { return offsets.empty() ? 0 : offsets.back(); }
+};
+
+// Ordered per-(sequence, KV head) selection read back from the device
+// (SelectionResult::blocks, engine.hpp:19-26).
+struct Selection {
+    std::size_t batch = 0, num_heads = 0;
+    std::vector<std::vector<std::size_t>> blocks;  // [b * num_heads + h], score-descending
+};
+
+// Device-resident decode attention over caller-owned paged KV caches; one
+// instance per device per host thread. Every call is
+// stream-ordered; only the download_* and *_host calls synchronise.
+class DecodeAttention {
+  public:
+    DecodeAttention(const EngineConfig& config, int device = 0) : config_(config) {
+        config_.validate();
+        const absp_config c = config_.to_abi();
+        check(absp_ctx_create(device, &c, &ctx_));
+    }
+    ~DecodeAttention() { absp_ctx_destroy(ctx_); }
+    DecodeAttention(const DecodeAttention&) = delete;
+    DecodeAttention& operator=(const DecodeAttention&) = delete;
+    DecodeAttention(DecodeAttention&& o) noexcept : config_(std::move(o.config_)), ctx_(o.ctx_) {
+        o.ctx_ = nullptr;
+    }
+
+    const EngineConfig& config() const { return config_; }
+    absp_ctx* handle() const { return ctx_; }
+
+    void set_assignment(uint32_t layer, const BlockAssignment& a) {
+        a.validate(config_);
+        std::vector<uint32_t> b(a.block_sizes.begin(), a.block_sizes.end());
+        check(absp_set_assignment(ctx_, layer, b.data()));
+    }
+    // k_pool/v_pool: bf16 [H][pool_pages][P][d] (device); page_table: u32
+    // [batch][max_pages] (device); seq_lens: host.
+    void bind(uint32_t layer, const void* k_pool, const void* v_pool, uint64_t pool_pages,
+              const uint32_t* page_table, uint32_t max_pages, const std::vector<uint32_t>& seq_lens) {
+        check(absp_kv_bind(ctx_, layer, k_pool, v_pool, pool_pages, page_table, max_pages,
+                           seq_lens.data(), uint32_t(seq_lens.size())));
+    }
+    void build_store(uint32_t layer, void* stream = nullptr) { check(absp_build_store(ctx_, layer, stream)); }
+    void select(uint32_t layer, const void* q, uint32_t* blocks, uint32_t stride, uint32_t* counts,
+                void* stream = nullptr) {
+        check(absp_select(ctx_, layer, q, blocks, stride, counts, stream));
+    }
+    void attend(uint32_t layer, const void* q, const uint32_t* blocks, uint32_t stride,
+                const uint32_t* counts, float* out, void* stream = nullptr) {
+        check(absp_attend(ctx_, layer, q, blocks, stride, counts, out, stream));
+    }
+    void decode_step(uint32_t layer, const void* q, float* out, void* stream = nullptr) {
+        check(absp_decode_step(ctx_, layer, q, out, stream));
+    }
+    void decode_step_host(uint32_t layer, const uint16_t* q_host, float* out_host, void* stream = nullptr) {
+        check(absp_decode_step_host(ctx_, layer, q_host, out_host, stream));
+    }
+    absp_layer_info layer_info(uint32_t layer) const {
+        absp_layer_info i{};
+        check(absp_get_layer_info(ctx_, layer, &i));
+        return i;
+    }
+    uint64_t launch_count() const { return absp_launch_count(ctx_); }
+
+    StoreSnapshot download_store(uint32_t layer, uint32_t seq) const {
+        const std::size_t H = config_.num_heads, d = config_.head_dim;
+        std::vector<uint64_t> off(H + 1);
+        check(absp_download_store(ctx_, layer, seq, off.data(), nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, nullptr, nullptr, nullptr));
+        StoreSnapshot s;
+        s.offsets.assign(off.begin(), off.end());
+        const std::size_t n = s.total_centroids();
+        const bool mm = config_.centroid_method == CentroidMethod::kMaxMin;
+        s.values.resize(n * d);
+        if (mm) s.values_min.resize(n * d);
+        if (config_.quant) {
+            s.codes.resize(n * d);
+            s.scales.resize(H * d);
+            s.zero_points.resize(H * d);
+            if (mm) {
+                s.codes_min.resize(n * d);
+                s.scales_min.resize(H * d);
+                s.zero_points_min.resize(H * d);
+            }
+        }
+        auto p = [](auto& v) { return v.empty() ? nullptr : v.data(); };
+        check(absp_download_store(ctx_, layer, seq, nullptr, p(s.values), p(s.values_min), p(s.codes),
+                                  p(s.codes_min), p(s.scales), p(s.zero_points), p(s.scales_min),
+                                  p(s.zero_points_min)));
+        return s;
+    }
+    // estimate_scores' flattened output for one sequence (engine.hpp:47-49).
+    std::vector<float> download_scores(uint32_t layer, uint32_t seq) const {
+        std::vector<uint64_t> off(config_.num_heads + 1);
+        check(absp_download_store(ctx_, layer, seq, off.data(), nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, nullptr, nullptr, nullptr));
+        std::vector<float> sc(off.back());
+        check(absp_download_scores(ctx_, layer, seq, sc.data()));
+        return sc;
+    }
+
+  private:
+    EngineConfig config_;
+    absp_ctx* ctx_ = nullptr;
+};
+
+}  // namespace absp
+
+#endif  // ABSP_HPP

@@ -142,23 +142,34 @@ class BlockAssignment:
 
     @staticmethod
     def load(path) -> "BlockAssignment":
-        """Assignment file format of the calibrator: one 'head block' pair per line,
-        '#' comments allowed (calibrator.cpp:285-311)."""
-        pairs = {}
-        for raw in open(path):
-            line = raw.split("#", 1)[0].strip()
-            if not line:
+        """read_assignment_file (calibrator.cpp:285-311): one 'head block_size' pair per
+        line, consecutive heads from 0, empty lines skipped; RuntimeError (the
+        reference's std::runtime_error) on anything else."""
+        try:
+            lines = open(path).read().split("\n")
+        except OSError:
+            raise RuntimeError(f"read_assignment_file: cannot open {path}") from None
+        sizes = []
+        for line in lines:
+            if line == "":
                 continue
             parts = line.split()
-            if len(parts) != 2:
-                raise InvalidArgument(f"assignment: malformed line '{raw.strip()}'")
-            h, b = int(parts[0]), int(parts[1])
-            if h in pairs:
-                raise InvalidArgument(f"assignment: duplicate head {h}")
-            pairs[h] = b
-        if sorted(pairs) != list(range(len(pairs))):
-            raise InvalidArgument("assignment: heads must be 0..H-1")
-        return BlockAssignment([pairs[h] for h in range(len(pairs))])
+            ok = len(parts) >= 2 and parts[0].isdigit() and parts[1].isdigit() and int(parts[0]) == len(sizes)
+            if not ok:
+                raise RuntimeError(f"read_assignment_file: malformed line '{line}' "
+                                   "(expected 'head block_size' with consecutive heads)")
+            if len(parts) > 2:
+                raise RuntimeError(f"read_assignment_file: trailing tokens on line '{line}'")
+            sizes.append(int(parts[1]))
+        if not sizes:
+            raise RuntimeError(f"read_assignment_file: empty file {path}")
+        return BlockAssignment(sizes)
+
+    def save(self, path) -> None:
+        """write_assignment_file (calibrator.cpp:277-283)."""
+        with open(path, "w") as f:
+            for h, b in enumerate(self.block_sizes):
+                f.write(f"{h} {b}\n")
 
     def num_heads(self) -> int:
         return len(self.block_sizes)

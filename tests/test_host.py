@@ -30,17 +30,23 @@ def test_build_offsets_matches_oracle():
 
 
 def test_assignment_file(tmp_path):
+    """read/write_assignment_file semantics (calibrator.cpp:277-311)."""
     p = tmp_path / "assignment.txt"
-    p.write_text("# head block\n0 16\n1 64\n2 32 # comment\n")
+    BlockAssignment([16, 64, 32]).save(p)
+    assert p.read_text() == "0 16\n1 64\n2 32\n"
+    p.write_text("0 16\n\n1 64\n2 32\n")
     a = BlockAssignment.load(p)
     assert a.block_sizes == [16, 64, 32]
     cfg = EngineConfig(num_heads=3)
     a.validate(cfg)
     with pytest.raises(InvalidArgument):
         BlockAssignment([16, 48, 32]).validate(cfg)
-    p.write_text("0 16\n0 32\n")
-    with pytest.raises(InvalidArgument):
-        BlockAssignment.load(p)
+    for bad in ("0 16\n0 32\n", "1 16\n", "0 16 7\n", "", "0 x\n", "# c\n0 16\n"):
+        p.write_text(bad)
+        with pytest.raises(RuntimeError):
+            BlockAssignment.load(p)
+    with pytest.raises(RuntimeError):
+        BlockAssignment.load(tmp_path / "missing.txt")
 
 
 @pytest.mark.parametrize("batch,heads,world", [(16, 8, 1), (16, 8, 2), (16, 8, 8), (64, 8, 8), (1, 8, 8), (1, 8, 2), (3, 8, 2)])
