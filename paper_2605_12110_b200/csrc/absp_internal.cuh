@@ -27,10 +27,19 @@ struct UnitDesc {
     uint64_t seg;        // first centroid slot of this unit (prefix sum of cap)
 };
 
-// Work item of the scoring kernel: a run of centroids of one unit.
+// Work item of the scoring kernel: centroids [start, end) of one unit.
 struct ScoreItem {
     uint32_t unit;
     uint32_t start;
+    uint32_t end;
+    uint32_t pad_;
+};
+// Scoring work split: CTA c scores items [item_begin[c], item_begin[c+1]), an
+// equal share of the layer's flattened centroids cut at unit boundaries.
+struct ScoreWork {
+    const ScoreItem* items;
+    const uint32_t* item_begin;  // [grid + 1]
+    uint32_t grid;
 };
 
 // Everything a kernel needs about one bound layer.
@@ -49,7 +58,7 @@ struct LayerView {
     const UnitDesc* desc;
     float* values;      // fp32 centroids [seg][d] (maxmin: max-array)
     float* values_min;  // maxmin min-array
-    uint32_t* codes;    // packed, per unit [words][cap]
+    uint32_t* codes;    // packed rows [seg][W], word order per code_word_pos
     uint32_t* codes_min;
     float* scales;      // [units][d]
     float* zps;
@@ -58,10 +67,45 @@ struct LayerView {
     float* scores;      // [seg]
 };
 
+// Packed code rows: centroid i of a unit occupies W = D*bits/32 consecutive words
+// (64 B at int4, d = 128; the reference's row [centroid][d] at bits/8 bytes per
+// code). Inside a row the 16-byte groups are XOR-swizzled by the centroid index,
+// so that a straight bulk copy of consecutive rows into shared memory can be read
+// one row per lane with conflict-free 16-byte loads: 8 consecutive rows cover all
+// 8 bank groups for every logical group g. Word w of row i sits at
+//     ((w / 4) ^ key(i)) * 4 + w % 4,  key(i) = (i >> (3 - log2 U)) & (U - 1),
+// U = W / 4 groups per row (W in {4, 8, 16, 32}).
+__host__ __device__ constexpr uint32_t code_row_key(uint32_t i, uint32_t W) {
+    return W <= 4 ? 0u : (i >> (W == 8 ? 2 : W == 16 ? 1 : 0)) & (W / 4 - 1);
+}
+__host__ __device__ constexpr uint32_t code_word_pos(uint32_t i, uint32_t w, uint32_t W) {
+    return (((w >> 2) ^ code_row_key(i, W)) << 2) | (w & 3u);
+}
+
+// Launch with programmatic stream serialisation (PDL): the kernel may begin while
+// the previous kernel of the stream finishes; it orders itself with griddep_wait()
+// (ptx.cuh). Works inside CUDA-graph capture (programmatic edges).
+template <typename... Exp, typename... Act>
+cudaError_t launch_pdl(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Act&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<Act&&>(args)...);
+}
+
 // Launch wrappers (each returns cudaGetLastError after the launch).
 cudaError_t launch_build_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches);
-cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreItem* items,
-                         uint32_t n_items, cudaStream_t s, int* launches);
+cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreWork& work, cudaStream_t s,
+                         int* launches);
+cudaError_t init_score_attributes();  // per device, once
 // Selected blocks resolved to pool pages, laid out by global attention chunk:
 // unit u's slot s = entry * (B/P) + page lives at index chunk_base[u] * ns + s, so
 // chunk w's slots are [w * ns, (w + 1) * ns).
@@ -82,10 +126,12 @@ struct AttendWork {
     const uint32_t* chunk_unit;  // [n_work] unit of each chunk
     const uint32_t* chunk_idx;   // [n_work] chunk index within its unit
     const uint32_t* chunk_base;  // [units + 1] first chunk of each unit
+    const uint32_t* unit_run;    // [units] first CTA of the unit | number of CTA runs << 16
     uint32_t n_work;             // total chunks
-    uint32_t slots_per_unit;     // partial slots reserved per unit (max chunks of a unit)
+    uint32_t max_runs;           // partial slots per unit = max_runs * kAttnSplits
     uint32_t* unit_done;         // [units] completion counters (zero between launches)
-    uint32_t grid;               // persistent CTAs (one per SM)
+    uint32_t grid;               // persistent CTAs: min(n_work, SMs); CTA c owns chunks
+                                 // [c * n_work / grid, (c + 1) * n_work / grid)
 };
 cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages,
                           const uint32_t* counts, const AttendWork& work,
@@ -101,7 +147,7 @@ constexpr uint32_t kAttnChunkRows = 128;
 // Consumer warps per attention CTA; each owns a 16-row split of every chunk with
 // its own online-softmax state and partials (partial slots per chunk).
 constexpr uint32_t kAttnSplits = 8;
-// Centroids per scoring CTA, see score.cu.
-constexpr uint32_t kScoreItemCentroids = 2048;
+// Resident scoring CTAs per SM (score.cu: 256 threads, <= 128 registers).
+constexpr uint32_t kScoreCtasPerSm = 2;
 
 }  // namespace absp

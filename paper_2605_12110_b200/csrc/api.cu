@@ -74,15 +74,16 @@ struct DevBuf {
 
 // Device-side attention work list (see AttendWork).
 struct WorkList {
-    DevBuf<uint32_t> chunk_unit, chunk_idx, chunk_base, unit_done;
+    DevBuf<uint32_t> chunk_unit, chunk_idx, chunk_base, unit_done, unit_run;
     DevBuf<uint32_t> page;    // resolved page list, [n_work][ns] (see PageList)
     DevBuf<uint16_t> valid;
-    uint32_t n_work = 0, slots = 0, ns = 0;
+    uint32_t n_work = 0, max_runs = 0, ns = 0, grid = 0;
     void release() {
         chunk_unit.release();
         chunk_idx.release();
         chunk_base.release();
         unit_done.release();
+        unit_run.release();
         page.release();
         valid.release();
     }
@@ -101,6 +102,7 @@ struct Layer {
     std::vector<uint32_t> seq_lens;
     std::vector<UnitDesc> desc;
     std::vector<ScoreItem> items;
+    std::vector<uint32_t> item_begin;
     uint64_t total_cap = 0, total_centroids = 0;
     uint32_t max_cap = 0, max_nblocks = 0, max_budget = 0, max_select = 0;
     uint32_t sel_stride = 0;
@@ -109,6 +111,7 @@ struct Layer {
 
     DevBuf<UnitDesc> d_desc;
     DevBuf<ScoreItem> d_items;
+    DevBuf<uint32_t> d_item_begin;
     DevBuf<float> values, values_min, scales, zps, scales_min, zps_min, scores;
     DevBuf<uint32_t> codes, codes_min;
     DevBuf<uint32_t> sel_blocks, sel_counts;
@@ -117,7 +120,7 @@ struct Layer {
     DevBuf<float> stage_out;
 
     void release() {
-        d_desc.release(); d_items.release();
+        d_desc.release(); d_items.release(); d_item_begin.release();
         values.release(); values_min.release(); scales.release(); zps.release();
         scales_min.release(); zps_min.release(); scores.release();
         codes.release(); codes_min.release();
@@ -191,49 +194,67 @@ uint32_t chunks_for(uint32_t entries, uint32_t block) {
 }
 
 // Builds the chunk list for units holding at most min(N, cap) entries (cap = K for
-// decode, blocks_stride for explicit selections) and sizes the partial buffers.
-absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t cap, WorkList& wl) {
+// decode, blocks_stride for explicit selections), the CTA runs of every unit under
+// the persistent attention grid, and sizes the partial buffers.
+absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t cap, int num_sms,
+                       WorkList& wl) {
     std::vector<uint32_t> base(l.desc.size() + 1, 0), unit_of, idx_of;
-    uint32_t slots = 1;
     for (size_t u = 0; u < l.desc.size(); ++u) {
         const UnitDesc& d = l.desc[u];
         const uint32_t entries = std::min(d.n_blocks, decode ? d.budget : cap);
         const uint32_t ch = std::max(chunks_for(entries, d.block), 1u);
         base[u + 1] = base[u] + ch;
-        slots = std::max(slots, ch);
         unit_of.insert(unit_of.end(), ch, uint32_t(u));
         for (uint32_t c = 0; c < ch; ++c) idx_of.push_back(c);
     }
     wl.n_work = base.back();
-    wl.slots = slots;
     wl.ns = kAttnChunkRows / P;  // page slots per chunk
+    wl.grid = std::min<uint32_t>(wl.n_work, uint32_t(num_sms));
+    // CTA c owns chunks [c * n_work / grid, (c + 1) * n_work / grid) (attend.cu)
+    auto cta_of = [&](uint32_t w) {
+        uint32_t c = uint32_t((uint64_t(w) * wl.grid) / wl.n_work);
+        while (c + 1 < wl.grid && (uint64_t(c + 1) * wl.n_work) / wl.grid <= w) ++c;
+        while (c > 0 && (uint64_t(c) * wl.n_work) / wl.grid > w) --c;
+        return c;
+    };
+    std::vector<uint32_t> run(l.desc.size());
+    wl.max_runs = 1;
+    for (size_t u = 0; u < l.desc.size(); ++u) {
+        const uint32_t first = cta_of(base[u]), last = cta_of(base[u + 1] - 1);
+        if (first > 0xffffu) return fail(ABSP_EINVAL, "attention grid above 65535 CTAs");
+        run[u] = first | ((last - first + 1) << 16);
+        wl.max_runs = std::max(wl.max_runs, last - first + 1);
+    }
     const size_t n_slots = size_t(wl.n_work) * wl.ns;
     ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
     ABSP_CUDA(wl.chunk_idx.ensure(idx_of.size()));
     ABSP_CUDA(wl.chunk_base.ensure(base.size()));
     ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
+    ABSP_CUDA(wl.unit_run.ensure(l.desc.size()));
     ABSP_CUDA(wl.page.ensure(n_slots));
     ABSP_CUDA(wl.valid.ensure(n_slots));
     ABSP_CUDA(cudaMemcpy(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(wl.unit_run.p, run.data(), run.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
     ABSP_CUDA(cudaMemset(wl.valid.p, 0, n_slots * 2));
-    // one partial slot per (chunk, consumer warp)
-    ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(slots) * kAttnSplits * 8 * D));
-    ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(slots) * kAttnSplits * 16));
+    // one partial slot per (unit, CTA run, consumer warp)
+    ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 8 * D));
+    ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 16));
     return ABSP_OK;
 }
 
-AttendWork work_view(const WorkList& wl, int num_sms) {
+AttendWork work_view(const WorkList& wl) {
     AttendWork w{};
     w.chunk_unit = wl.chunk_unit.p;
     w.chunk_idx = wl.chunk_idx.p;
     w.chunk_base = wl.chunk_base.p;
+    w.unit_run = wl.unit_run.p;
     w.n_work = wl.n_work;
-    w.slots_per_unit = wl.slots;
+    w.max_runs = wl.max_runs;
     w.unit_done = wl.unit_done.p;
-    w.grid = uint32_t(num_sms);
+    w.grid = wl.grid;
     return w;
 }
 
@@ -315,6 +336,7 @@ absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) 
         return fail(ABSP_ECUDA, "this library is built for sm_100a (B200); device is sm_" +
                                     std::to_string(prop.major) + std::to_string(prop.minor));
     ABSP_CUDA(init_attend_attributes());
+    ABSP_CUDA(init_score_attributes());
     auto* ctx = new absp_ctx;
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
@@ -423,10 +445,30 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
             l->max_nblocks = std::max(l->max_nblocks, d.n_blocks);
             l->max_budget = std::max(l->max_budget, d.budget);
             l->max_select = std::max(l->max_select, sel);
-            const uint32_t u = uint32_t(l->desc.size());
-            for (uint32_t s = 0; s < d.n_blocks; s += kScoreItemCentroids) l->items.push_back({u, s});
             l->desc.push_back(d);
         }
+    }
+    // Scoring split: CTA c gets the flattened centroid range [c*T/grid, (c+1)*T/grid),
+    // cut into per-unit items, so every CTA scores the same number of centroids
+    // whatever the block sizes (no partial last wave).
+    {
+        const uint32_t grid = uint32_t(std::max<uint64_t>(
+            1, std::min<uint64_t>(uint64_t(ctx->num_sms) * kScoreCtasPerSm, l->total_centroids)));
+        l->item_begin.assign(grid + 1, 0);
+        uint32_t u = 0;
+        uint64_t ubase = 0;  // flattened index of unit u's first centroid
+        for (uint32_t c = 0; c < grid; ++c) {
+            const uint64_t lo = l->total_centroids * c / grid, hi = l->total_centroids * (c + 1) / grid;
+            l->item_begin[c] = uint32_t(l->items.size());
+            uint64_t pos = lo;
+            while (pos < hi) {
+                while (ubase + l->desc[u].n_blocks <= pos) ubase += l->desc[u++].n_blocks;
+                const uint64_t e = std::min<uint64_t>(hi, ubase + l->desc[u].n_blocks);
+                l->items.push_back({u, uint32_t(pos - ubase), uint32_t(e - ubase), 0u});
+                pos = e;
+            }
+        }
+        l->item_begin[grid] = uint32_t(l->items.size());
     }
     const size_t units = l->desc.size();
     const size_t D = c.head_dim;
@@ -434,6 +476,7 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     const size_t W = words_per_centroid(c);
     ABSP_CUDA(l->d_desc.ensure(units));
     ABSP_CUDA(l->d_items.ensure(l->items.size()));
+    ABSP_CUDA(l->d_item_begin.ensure(l->item_begin.size()));
     ABSP_CUDA(l->values.ensure(l->total_cap * D));
     if (mm) ABSP_CUDA(l->values_min.ensure(l->total_cap * D));
     if (c.quant_bits) {
@@ -452,10 +495,12 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     ABSP_CUDA(l->sel_counts.ensure(units));
     for (auto& kv : l->attend_work) kv.second.release();
     l->attend_work.clear();
-    st = build_work(*l, c.head_dim, c.page_size, true, 0, l->step_work);
+    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
     if (st != ABSP_OK) return st;
     ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
+                         cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(l->d_item_begin.p, l->item_begin.data(), l->item_begin.size() * 4,
                          cudaMemcpyHostToDevice));
     l->bound = true;
     l->built = false;
@@ -482,8 +527,8 @@ static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* b
                              uint32_t stride, uint32_t* counts, cudaStream_t s) {
     const LayerView v = view_of(ctx, *l);
     int n = 0;
-    cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), l->d_items.p,
-                                 uint32_t(l->items.size()), s, &n);
+    const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1)};
+    cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), sw, s, &n);
     if (e == cudaSuccess)
         e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), s, &n);
     ctx->launches += n;
@@ -494,7 +539,7 @@ static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* b
 static absp_status do_attend_step(absp_ctx* ctx, Layer* l, const void* q, float* out, cudaStream_t s) {
     int n = 0;
     cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->step_work.pages(),
-                                  l->sel_counts.p, work_view(l->step_work, ctx->num_sms), l->part_o.p,
+                                  l->sel_counts.p, work_view(l->step_work), l->part_o.p,
                                   l->part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
@@ -530,7 +575,7 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     // per unit; built once per stride (the first call for a new stride allocates).
     auto it = l->attend_work.find(blocks_stride);
     if (it == l->attend_work.end()) {
-        st = build_work(*l, ctx->cfg.head_dim, ctx->cfg.page_size, false, blocks_stride,
+        st = build_work(*l, ctx->cfg.head_dim, ctx->cfg.page_size, false, blocks_stride, ctx->num_sms,
                         l->attend_work[blocks_stride]);
         if (st != ABSP_OK) return st;
         it = l->attend_work.find(blocks_stride);
@@ -541,7 +586,7 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     cudaError_t e = launch_resolve_pages(v, blocks, blocks_stride, counts, it->second.pages(), s, &n);
     if (e == cudaSuccess)
         e = launch_attend(v, static_cast<const uint16_t*>(q), it->second.pages(), counts,
-                          work_view(it->second, ctx->num_sms), l->part_o.p, l->part_ml.p, out, s, &n);
+                          work_view(it->second), l->part_o.p, l->part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
@@ -666,11 +711,11 @@ absp_status absp_download_store(absp_ctx* ctx, uint32_t layer, uint32_t seq, uin
                 uint8_t* dst = a ? codes_min : codes;
                 if (!dst) continue;
                 const uint32_t* src = (a ? l->codes_min.p : l->codes.p) + d.seg * W;
-                words.resize(size_t(W) * d.cap);
+                words.resize(size_t(W) * n);
                 ABSP_CUDA(cudaMemcpy(words.data(), src, words.size() * 4, cudaMemcpyDeviceToHost));
                 for (size_t i = 0; i < n; ++i)
                     for (uint32_t ch = 0; ch < D; ++ch) {
-                        const uint32_t w = words[size_t(ch / cpw) * d.cap + i];
+                        const uint32_t w = words[i * W + code_word_pos(uint32_t(i), ch / cpw, W)];
                         dst[(off + i) * D + ch] = uint8_t((w >> ((ch % cpw) * bits)) & ((1u << bits) - 1u));
                     }
             }
@@ -724,6 +769,16 @@ uint64_t absp_launch_count(absp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 // stamps (uint64 globaltimer ns, [160 CTAs][256 slots]) to host memory.
 namespace absp {
 cudaError_t debug_attn_trace(void* dst, size_t bytes);
+cudaError_t debug_score_trace(void* dst, size_t bytes);
+cudaError_t debug_topk_trace(void* dst, size_t bytes);
+}
+extern "C" absp_status absp_debug_topk_trace(void* dst, size_t bytes) {
+    cudaError_t e = absp::debug_topk_trace(dst, bytes);
+    return e == cudaSuccess ? ABSP_OK : cuda_fail(e, "debug_topk_trace");
+}
+extern "C" absp_status absp_debug_score_trace(void* dst, size_t bytes) {
+    cudaError_t e = absp::debug_score_trace(dst, bytes);
+    return e == cudaSuccess ? ABSP_OK : cuda_fail(e, "debug_score_trace");
 }
 extern "C" absp_status absp_debug_attn_trace(void* dst, size_t bytes) {
     cudaError_t e = absp::debug_attn_trace(dst, bytes);

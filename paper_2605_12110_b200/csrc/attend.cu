@@ -39,6 +39,7 @@
 // (P <= 16). Softmax is permutation-invariant over rows and P uses the same
 // permutation, so the result is unchanged.
 #include "absp_internal.cuh"
+#include "ptx.cuh"
 
 #include <math.h>
 
@@ -72,35 +73,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define ATTN_TRACE(slot) do {} while (0)
 #endif
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
     uint32_t old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -170,7 +142,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                                                       const uint32_t* __restrict__ chunk_unit,
                                                       const uint32_t* __restrict__ chunk_idx,
                                                       const uint32_t* __restrict__ chunk_base,
-                                                      uint32_t n_work, uint32_t slots_per_unit,
+                                                      const uint32_t* __restrict__ unit_run,
+                                                      uint32_t n_work, uint32_t max_runs,
                                                       float* __restrict__ part_o,
                                                       float* __restrict__ part_ml,
                                                       uint32_t* __restrict__ unit_done,
@@ -194,10 +167,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             mbar_init(smem_u32(&sh.full[s]), 1);
             mbar_init(smem_u32(&sh.empty[s]), kWarps);  // every consumer warp
         }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        mbar_fence_init();
     }
     if (tid == 0) ATTN_TRACE(0);
+    griddep_launch_dependents();
     __syncthreads();
+    griddep_wait();  // page lists, q, partial buffers and unit counters are step data
 
     if (warp == kWarps) {
         // ============================ producer ================================
@@ -305,80 +280,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // partial slot of (unit, first chunk of a run, warp)
-    auto slot_of = [&](uint32_t unit, uint32_t chunk, uint32_t wp) -> size_t {
-        return (size_t(unit) * slots_per_unit + chunk) * kWarps + wp;
+    // Partial slot of (unit, run, warp). A run is the part of a unit's chunks one CTA
+    // processes (CTA ranges are contiguous, so run r of unit u belongs to CTA
+    // first_cta(u) + r); every warp of that CTA writes exactly one partial per run.
+    auto slot_of = [&](uint32_t unit, uint32_t run, uint32_t wp) -> size_t {
+        return (size_t(unit) * max_runs + run) * kWarps + wp;
     };
 
     // LSE merge of every partial of unit mu for query head h into `out` (one warp).
-    // Loads are issued in bulk: the (m, l) of all slots (lanes stride the slots),
-    // then the o rows of the live slots four at a time.
+    // Every slot of the unit's runs is written each step, so the o rows are loaded
+    // without waiting for (m, l): lanes own D/32 contiguous channels, windows of 32
+    // slots, o loads 8 slots at a time, all independent — about one L2 round trip.
     auto merge = [&](uint32_t mu, uint32_t h) {
         constexpr int PER = D / 32;
-        constexpr int MAXW = 8;  // 32-slot windows held in registers (<= 256 slots)
-        const uint32_t nslots = (chunk_base[mu + 1] - chunk_base[mu]) * kWarps;
-        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16;
-        const float* pou = part_o + slot_of(mu, 0, 0) * 8 * D;
+        const uint32_t nslots = (unit_run[mu] >> 16) * kWarps;
+        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16 + h * 2;
+        const float* pou = part_o + (slot_of(mu, 0, 0) * 8 + h) * D + lane * PER;
         float acc[PER];
 #pragma unroll
         for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
-        float lsum = 0.0f, M = -INFINITY;
-        for (uint32_t base = 0; base < nslots; base += 32 * MAXW) {
-            float mv[MAXW], lv[MAXW];
-#pragma unroll
-            for (int k = 0; k < MAXW; ++k) {
-                const uint32_t c = base + k * 32 + lane;
-                mv[k] = c < nslots ? __ldcg(mlu + c * 16 + h * 2) : -INFINITY;
-                lv[k] = c < nslots ? __ldcg(mlu + c * 16 + h * 2 + 1) : 0.0f;
-            }
-            float Mw = -INFINITY;
-#pragma unroll
-            for (int k = 0; k < MAXW; ++k) Mw = fmaxf(Mw, mv[k]);
+        float lpart = 0.0f, M = -INFINITY;
+        for (uint32_t base = 0; base < nslots; base += 32) {
+            const uint32_t n = min(32u, nslots - base);
+            const float mv = lane < n ? __ldcg(mlu + (base + lane) * 16) : -INFINITY;
+            const float lv = lane < n ? __ldcg(mlu + (base + lane) * 16 + 1) : 0.0f;
+            float Mw = mv;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, off));
-            if (Mw == -INFINITY) continue;
-            // rescale what was accumulated from earlier windows
             const float Mn = fmaxf(M, Mw);
+            if (Mn == -INFINITY) continue;  // nothing live so far (warp-uniform)
             const float r = M == -INFINITY ? 0.0f : exp2f(M - Mn);
-            lsum *= r;
+            lpart *= r;
 #pragma unroll
             for (int i = 0; i < PER; ++i) acc[i] *= r;
             M = Mn;
+            const float wl = mv == -INFINITY ? 0.0f : exp2f(mv - M);  // weight of slot base + lane
+            lpart += wl * lv;
+            for (uint32_t s0 = 0; s0 < n; s0 += 8) {
+                float v[8][PER];
 #pragma unroll
-            for (int k = 0; k < MAXW; ++k) {
-                const float wgt = mv[k] == -INFINITY ? 0.0f : exp2f(mv[k] - M);
-                lsum += wgt * lv[k];
-                uint32_t live = __ballot_sync(0xffffffffu, wgt != 0.0f);
-                while (live) {
-                    uint32_t src[4];
-                    float wc[4];
+                for (int j = 0; j < 8; ++j) {
+                    const float* src = pou + size_t(base + s0 + j) * 8 * D;
+                    if (s0 + j < n) {
+                        if (PER == 4) {
+                            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+                            v[j][0] = t.x; v[j][1] = t.y; v[j][2 % PER] = t.z; v[j][3 % PER] = t.w;
+                        } else {
+                            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+                            v[j][0] = t.x; v[j][1 % PER] = t.y;
+                        }
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        src[j] = live ? __ffs(live) - 1 : 32u;
-                        live = live ? live & (live - 1) : 0u;
-                        wc[j] = __shfl_sync(0xffffffffu, wgt, src[j] & 31);
-                        if (src[j] == 32u) wc[j] = 0.0f;
+                        for (int i = 0; i < PER; ++i) v[j][i] = 0.0f;
                     }
-                    float v[4][PER];
+                }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float* pc = pou + ((base + k * 32 + (src[j] & 31)) * 8 + h) * D;
+                for (int j = 0; j < 8; ++j) {
+                    const float wj = __shfl_sync(0xffffffffu, wl, (s0 + j) & 31);
 #pragma unroll
-                        for (int i = 0; i < PER; ++i) v[j][i] = src[j] == 32u ? 0.0f : __ldcg(pc + lane + 32 * i);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-#pragma unroll
-                        for (int i = 0; i < PER; ++i) acc[i] += wc[j] * v[j][i];
+                    for (int i = 0; i < PER; ++i) acc[i] += wj * v[j][i];
                 }
             }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
-        const float inv = 1.0f / lsum;
-        float* dst = out + (size_t(mu) * G + h) * D;  // out is [b][h*G + g][d], u = b*H + h
-#pragma unroll
-        for (int i = 0; i < PER; ++i) dst[lane + 32 * i] = acc[i] * inv;
+        for (int off = 16; off > 0; off >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, off);
+        const float inv = 1.0f / lpart;
+        float* dst = out + (size_t(mu) * G + h) * D + lane * PER;  // out is [b][h*G + g][d], u = b*H + h
+        if (PER == 4)
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[0] * inv, acc[1 % PER] * inv, acc[2 % PER] * inv,
+                                                          acc[3 % PER] * inv);
+        else
+            *reinterpret_cast<float2*>(dst) = make_float2(acc[0] * inv, acc[1 % PER] * inv);
     };
 
     // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count its
@@ -390,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
-        const size_t slot = slot_of(cur_u, seg_first, warp);
+        const size_t slot = slot_of(cur_u, blockIdx.x - (unit_run[cur_u] & 0xffffu), warp);
         float* po = part_o + slot * 8 * D;
         float* ml = part_ml + slot * 16;
 #pragma unroll
@@ -410,12 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             ml[(2 * t4) * 2 + 1] = lsum[0];
             ml[(2 * t4 + 1) * 2] = m_run[1];
             ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
-        }
-        // the run's other chunks carry no partial of their own (for this warp)
-        for (uint32_t c = seg_first + 1 + lane / 8; c <= seg_last; c += 4) {
-            float* mc = part_ml + slot_of(cur_u, c, warp) * 16;
-            mc[(lane % 8) * 2] = -INFINITY;
-            mc[(lane % 8) * 2 + 1] = 0.0f;
         }
         // completion counting: the release publishes this warp's partials to the warp
         // that completes the unit, whose acquire makes every partial visible to it
@@ -597,16 +563,14 @@ cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList&
                           float* part_ml, float* out, cudaStream_t s, int* launches) {
     (void)counts;  // chunk page lists carry the selection (empty slots have valid = 0)
     const size_t smem = attend_smem_bytes(L.D, L.P);
-    const uint32_t grid = wk.n_work < wk.grid ? wk.n_work : wk.grid;
+    const uint32_t grid = wk.grid;  // = min(n_work, SMs): the CTA runs in unit_run assume it
     if (grid == 0) return cudaSuccess;
     if (L.D == 64)
-        k_attn<64><<<grid, kThreads, smem, s>>>(L, q, pages, wk.chunk_unit, wk.chunk_idx, wk.chunk_base,
-                                                wk.n_work, wk.slots_per_unit, part_o, part_ml, wk.unit_done,
-                                                out);
+        launch_pdl(k_attn<64>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, wk.chunk_unit, wk.chunk_idx,
+                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, part_o, part_ml, wk.unit_done, out);
     else
-        k_attn<128><<<grid, kThreads, smem, s>>>(L, q, pages, wk.chunk_unit, wk.chunk_idx, wk.chunk_base,
-                                                 wk.n_work, wk.slots_per_unit, part_o, part_ml, wk.unit_done,
-                                                 out);
+        launch_pdl(k_attn<128>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, wk.chunk_unit, wk.chunk_idx,
+                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, part_o, part_ml, wk.unit_done, out);
     ++*launches;
     return cudaGetLastError();
 }

@@ -9,10 +9,10 @@
 // HBM layout written here (per layer, capacity-reserved per unit u=(b,h)):
 //   values   fp32 [seg_u + i][D]                 (CentroidStore::values)
 //   scales   fp32 [u][D], zps fp32 [u][D]         (per (head, channel) params)
-//   codes    u32  [seg_u * W + w * cap_u + i]     W = D*bits/32 words/centroid,
-//            word w holds channels w*(32/bits) .. +32/bits-1, low bits first.
-//            Word-major per unit so that the scorer's thread-per-centroid loads
-//            are fully coalesced (one 128 B line per warp per word).
+//   codes    u32  [(seg_u + i) * W + code_word_pos(i, w, W)]   W = D*bits/32
+//            words per centroid row; word w holds channels w*(32/bits) ..
+//            +32/bits-1, low bits first. Rows are contiguous per unit so the
+//            scorer bulk-copies runs of rows into shared memory (score.cu).
 #include "absp_internal.cuh"
 
 #include <math.h>
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(32 * (D * BITS / 32)) k_encode(LayerView L, co
         }
         word |= uint32_t(q) << (k * BITS);
     }
-    codes[du.seg * W + size_t(w) * du.cap + i] = word;
+    codes[(du.seg + i) * W + code_word_pos(i, w, W)] = word;
 }
 
 template <int D>

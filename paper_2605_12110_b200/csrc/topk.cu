@@ -25,6 +25,7 @@
 //      reference's populate_page_spans, engine.cpp:271-283) for the attention
 //      producer: page id and valid-row count per page slot.
 #include "absp_internal.cuh"
+#include "ptx.cuh"
 
 namespace absp {
 namespace {
@@ -34,6 +35,20 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSort = 2048;   // max K
 constexpr int kMaxSteps = 4096;  // max (N-1)/32 warp-steps for index tie ranking
 constexpr int kCompact = 2048;   // compaction capacity (keys matching the prefix)
+
+// Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE).
+#ifdef ABSP_ATTN_TRACE
+constexpr int kTopkTraceSlots = 8;
+__device__ unsigned long long g_topk_trace[1024 * kTopkTraceSlots];
+__device__ __forceinline__ void topk_trace(int slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_topk_trace[blockIdx.x * kTopkTraceSlots + slot] = t;
+}
+#define TOPK_TRACE(slot) do { if (threadIdx.x == 0) topk_trace(slot); } while (0)
+#else
+#define TOPK_TRACE(slot) do {} while (0)
+#endif
 
 __device__ __forceinline__ uint32_t order_key(float f) {
     uint32_t u = __float_as_uint(f);
@@ -117,6 +132,7 @@ template <bool REG, int ITEMS>
 __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
                                                    uint32_t* counts, PageList pages) {
     __shared__ TopkSmem sm;
+    TOPK_TRACE(0);
     const uint32_t u = blockIdx.x;
     const UnitDesc du = L.desc[u];
     const uint32_t N = du.n_blocks;
@@ -128,6 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     const uint32_t nsteps = (n_cand + 31) / 32;
     const int my_items = REG ? ITEMS : int((nsteps + kWarps - 1 - warp) / kWarps);
 
+    griddep_launch_dependents();
+    griddep_wait();  // the scores are written by the scoring kernel of this step
     Keys<REG, ITEMS> keys;
     keys.sc = sc;
     keys.n_cand = n_cand;
@@ -157,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     // groups of 4 keys. At least K-1 groups have a maximum >= x, so the candidates
     // {key >= x} contain the whole top-(K-1); typically only a little more than K-1
     // of them exist. They are compacted and ordered exactly among themselves.
+    TOPK_TRACE(1);
     if (REG && N > K && K > 1) {
         constexpr int GS = ITEMS >= 4 ? 4 : 1;
         constexpr int NG = ITEMS / GS;
@@ -228,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
             pmask |= ((1u << nbits) - 1u) << shift;
             lo_bit = shift;
         }
+        TOPK_TRACE(2);
         const uint32_t x = prefix;  // bucket lower edge: low bits zero
         uint32_t c = 0;
 #pragma unroll
@@ -254,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
                 }
             }
             __syncthreads();
+            TOPK_TRACE(3);
             const unsigned long long ct = (uint64_t(order_key(sc[N - 1])) << 32) | uint32_t(~(N - 1));
             uint32_t* out = blocks + size_t(u) * stride;
             if (C <= 256) {
@@ -295,9 +316,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
             __syncthreads();
             if (threadIdx.x == 0) {
                 out[sm.nsel] = N - 1;  // the trailing block sits after every larger winner
+                TOPK_TRACE(4);
                 counts[u] = K;
             }
             resolve_pages(L, du, u, K, out, pages);
+            TOPK_TRACE(5);
             return;
         }
         // too many candidates (heavy ties near the threshold): exact path below
@@ -553,6 +576,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
 
 }  // namespace
 
+#ifdef ABSP_ATTN_TRACE
+cudaError_t debug_topk_trace(void* dst, size_t bytes) {
+    return cudaMemcpyFromSymbol(dst, g_topk_trace, bytes);
+}
+#endif
+
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
                         cudaStream_t s, int* launches) {
@@ -560,7 +589,7 @@ cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_b
         return cudaErrorInvalidValue;
     const uint32_t per_thread = (max_nblocks + kThreads - 1) / kThreads;
     const dim3 grid(L.units);
-#define ABSP_TOPK(REG, IT) k_topk<REG, IT><<<grid, kThreads, 0, s>>>(L, blocks, stride, counts, pages)
+#define ABSP_TOPK(REG, IT) launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages)
     if (per_thread <= 1) ABSP_TOPK(true, 1);
     else if (per_thread <= 2) ABSP_TOPK(true, 2);
     else if (per_thread <= 4) ABSP_TOPK(true, 4);
@@ -577,6 +606,8 @@ cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_b
 // Page resolution for an explicit (caller-provided) selection: absp_attend.
 __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks, uint32_t stride,
                                 const uint32_t* __restrict__ counts, PageList pages) {
+    griddep_launch_dependents();
+    griddep_wait();  // blocks / counts may come from the previous kernel
     const uint32_t u = blockIdx.x;
     const UnitDesc du = L.desc[u];
     const uint32_t ppb = du.block / L.P;
@@ -605,7 +636,7 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
                                  const uint32_t* counts, const PageList& pages, cudaStream_t s,
                                  int* launches) {
-    k_resolve_pages<<<L.units, 256, 0, s>>>(L, blocks, stride, counts, pages);
+    launch_pdl(k_resolve_pages, dim3(L.units), dim3(256), 0, s, L, blocks, stride, counts, pages);
     ++*launches;
     return cudaGetLastError();
 }
