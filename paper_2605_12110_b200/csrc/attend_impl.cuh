@@ -1,0 +1,640 @@
+// Shared by attend.cu (k_attn) and step.cu (the fused decode step).
+#pragma once
+// Kernel 3: variable-block-size sparse paged flash-decoding with split-KV
+// partials and a fused log-sum-exp merge (sm_100a).
+//
+// Reference: sparse_attention / attend_rows (engine.cpp:180-210, 285-327):
+// softmax(q . k / sqrt(d)) . v over the rows of the selected blocks, rows
+// resolved through the page table (block_to_pages, kv_cache.cpp:118-138). The
+// PageSpan objects of populate_page_spans (engine.cpp:271-283) become the page
+// list the top-k kernel resolves; no gather copy, no per-step allocation.
+//
+// Work: the selection of unit u = (b, h) is cut into chunks of E = 128/B
+// consecutive entries (128 rows = 128/P whole pages), and a unit's chunks into
+// pieces of up to kAttnPieceChunks chunks. A persistent grid claims pieces in unit
+// order from a shared counter (dynamic balancing: every CTA streams until the list
+// is exhausted, whatever its share of bandwidth), so the whole GPU works on the
+// earliest units first — which is what lets the fused decode step (step.cu) start
+// attending a sequence while later sequences are still being scored.
+//
+// CTA = 8 consumer warps + 1 producer warp, 3-stage mbarrier ring of 64 KB stages:
+//   producer : lane s handles page slot s of the chunk two ahead (page list
+//              prefetched with independent loads) and issues one cp.async.bulk per
+//              page for K and V — the TMA bulk-copy engine, 1 instruction per 1-4 KB
+//              page — plus one for the unit's G query rows, completing on the
+//              stage's full barrier. In the fused step it first waits for the
+//              unit's "selection published" flag (acquire). (A copy-only probe of this pipeline streams
+//              scattered 4 KB pages at 97% of measured HBM bandwidth.)
+//   consumers: warp w owns rows [16w, 16w+16) of every chunk and is an independent
+//              split with its own fp32 online-softmax state: S^T = K Q^T on
+//              mma.m16n8k16 (M = 16 KV rows, N = 8 query heads of the GQA group,
+//              K = d), P through a per-warp smem tile (bf16 hi + bf16 residual,
+//              ~16 mantissa bits), O^T += V^T P^T (M = 16 channels x d/16 tiles,
+//              N = 8 heads, K = the warp's 16 rows). A warp takes its fragments
+//              into registers and releases the stage before the softmax/PV math, so
+//              a stage is held only for QK + ldmatrix. No cross-warp barrier: at the
+//              end of a piece each warp writes its own partial (m, l, o[G][d]) and
+//              counts its chunks; the warp completing a unit queues its LSE merge,
+//              done by the CTA's warps after the chunk loop (one warp per (unit,
+//              head), one L2 round trip).
+//
+// Bank conflicts without TMA swizzle: a page lands contiguously in smem, so rows
+// of one page are 256 B apart (same banks). Page slots are staggered by 16 B and
+// logical row i of a chunk is (slot i % NS, row i / NS), NS = 128/P: the 8 rows of
+// an ldmatrix phase come from 8 different slots, i.e. 8 distinct 16 B bank groups
+// (P <= 16). Softmax is permutation-invariant over rows and P uses the same
+// permutation, so the result is unchanged.
+#include "absp_internal.cuh"
+#include "ptx.cuh"
+
+#include <math.h>
+
+namespace absp {
+namespace attn {
+
+constexpr int kRows = kAttnChunkRows;    // 128 rows per chunk / stage
+constexpr int kWarps = kAttnSplits;      // consumer warps = splits per chunk (8)
+constexpr int kConsumers = 32 * kWarps;
+constexpr int kThreads = kConsumers + 64;  // + 1 producer warp + 1 bookkeeping warp
+constexpr int kFlushSlots = 4;             // piece flushes in flight to the bookkeeper
+constexpr int kStages = 3;
+constexpr int kWarpRows = kRows / kWarps;  // 16
+constexpr int kPStride = kWarpRows + 8;    // bf16 row stride of a P tile (bank-conflict free)
+constexpr int kMaxSlots = kRows;           // P >= 1
+
+// Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
+// globaltimer stamps of the producer's issues, warp 0's data arrivals / releases,
+// flushes and merges. Read back with absp_debug_attn_trace.
+#ifdef ABSP_ATTN_TRACE
+namespace {
+constexpr int kTraceSlots = 256;
+__device__ unsigned long long g_attn_trace[160 * kTraceSlots];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+}  // namespace
+#define ATTN_TRACE(slot) \
+    do { if (blockIdx.x < 160 && (slot) < kTraceSlots) g_attn_trace[blockIdx.x * kTraceSlots + (slot)] = gtime(); } while (0)
+#else
+#define ATTN_TRACE(slot) do {} while (0)
+#endif
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
+                                        uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
+                                          uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint16_t f2bf(float f) {
+    uint32_t u = __float_as_uint(f);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return uint16_t(u >> 16);
+}
+
+struct StageMeta {
+    __align__(16) uint16_t q[8 * 128];  // the chunk's unit's G query rows (bf16)
+    uint32_t unit;              // 0xffffffff: no more work (sentinel)
+    uint32_t chunk;             // bit 31: some row of the chunk carries no token
+    uint32_t piece;
+    uint8_t valid[kMaxSlots];   // valid rows per page slot (0..P; P <= 128)
+};
+
+template <int D>
+struct SmemHead {  // fixed-size part after the stage tiles
+    unsigned long long full[kStages];
+    unsigned long long empty[kStages];
+    StageMeta meta[kStages];
+    // piece flushes: consumer warps -> bookkeeping warp (unit, chunks of the piece)
+    unsigned long long flush_full[kFlushSlots];
+    unsigned long long flush_empty[kFlushSlots];
+    uint32_t flush_unit[kFlushSlots];
+    uint32_t flush_chunks[kFlushSlots];
+    uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
+};
+
+__host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
+    return ((kRows * D * 2 + (kRows / P) * 16) + 127) / 128 * 128;
+}
+
+// Everything one attention CTA needs (kernel parameter of k_attn and k_step).
+struct AttnArgs {
+    LayerView L;
+    const uint16_t* q;
+    PageList pages;
+    const uint32_t* chunk_base;   // [units + 1] global chunk index of each unit's chunk 0
+    const uint32_t* piece_unit;   // [n_pieces] unit of each piece (unit order)
+    const uint32_t* piece_info;   // [n_pieces] first chunk | chunk count << 16
+    const uint32_t* unit_piece;   // [units] first piece | piece count << 16
+    uint32_t n_pieces;
+    uint32_t max_pieces;          // partial slots per unit = max_pieces * kWarps
+    uint32_t ncta;                // CTAs taking part (for the exit count)
+    float* part_o;
+    float* part_ml;
+    uint32_t* unit_done;          // [units] chunk completion counters (zero between steps)
+    uint32_t* work;               // [2] piece claim counter, CTA exit counter (zero between steps)
+    uint32_t* ready;              // fused step: [units] selection published (else null)
+    uint32_t* scored;             // fused step: [units] scorer completion counters (else null)
+    float* out;
+};
+
+template <int D>
+__device__ __forceinline__ void attn_cta(const AttnArgs& a, unsigned char* smem) {
+    constexpr int MT = D / 16;  // 16-channel PV m-tiles (each warp covers every channel)
+    const LayerView& L = a.L;
+    const uint16_t* __restrict__ q = a.q;
+    const PageList& pages = a.pages;
+    float* __restrict__ part_o = a.part_o;
+    float* __restrict__ part_ml = a.part_ml;
+    float* __restrict__ out = a.out;
+    const uint32_t P = L.P;
+    const uint32_t NS = kRows / P;  // page slots per chunk
+    const uint32_t TB = tile_bytes(D, P);
+    const uint32_t slot_stride = P * D * 2 + 16;
+    SmemHead<D>& sh = *reinterpret_cast<SmemHead<D>*>(smem + kStages * 2 * TB);
+    const uint32_t smem_base = smem_u32(smem);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int i = 0; i < kFlushSlots; ++i) {
+            mbar_init(smem_u32(&sh.flush_full[i]), kWarps);
+            mbar_init(smem_u32(&sh.flush_empty[i]), 1);
+        }
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(smem_u32(&sh.full[s]), 1);
+            mbar_init(smem_u32(&sh.empty[s]), kWarps);  // every consumer warp
+        }
+        mbar_fence_init();
+    }
+    if (tid == 0) ATTN_TRACE(0);
+    __syncthreads();
+
+    if (warp == kWarps) {
+        // ============================ producer ================================
+        // Pieces are claimed from the shared counter as the previous one runs out; a chunk's page list
+        // (resolved by the top-k, laid out by global chunk index) is fetched one chunk
+        // ahead of its copy issue. Lane k*32+l owns page slot k*32+l (NS <= 128 slots
+        // -> up to 4 per lane).
+        constexpr int SPL = kMaxSlots / 32;
+        struct Job {
+            uint32_t u, c, p, gp[SPL], vl[SPL];
+        };
+        // The next piece is claimed as the current one starts (one piece held in
+        // reserve, so the claim's round trip is hidden behind the current piece);
+        // lane 0 keeps the claim's result and it is only read at the piece boundary.
+        // CTA c starts with piece c without claiming; claims return pieces from ncta on.
+        uint32_t claim = 0;
+        uint32_t cur_p = blockIdx.x;
+        uint32_t cur_u = 0, cur_c0 = 0, cur_n = 0, cur_i = 0;
+        auto start_piece = [&]() {
+            if (lane == 0) claim = atomicAdd(a.work, 1u) + a.ncta;  // the reserve piece
+            cur_u = __ldg(a.piece_unit + cur_p);
+            const uint32_t info = __ldg(a.piece_info + cur_p);
+            cur_c0 = info & 0xffffu;
+            cur_n = info >> 16;
+            cur_i = 0;
+            if (a.ready)  // fused step: wait until the unit's selection is published
+                while (ld_acquire(a.ready + cur_u) == 0u) __nanosleep(64);
+        };
+        if (cur_p < a.n_pieces) start_piece();
+        auto fetch = [&](Job& j) -> bool {
+            if (cur_p >= a.n_pieces) return false;
+            j.u = cur_u;
+            j.p = cur_p;
+            j.c = cur_c0 + cur_i;
+            const size_t base = size_t(__ldg(a.chunk_base + cur_u) + j.c) * NS;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const uint32_t s = k * 32 + lane;
+                j.gp[k] = s < NS ? __ldcg(pages.page + base + s) : 0u;
+                j.vl[k] = s < NS ? __ldcg(pages.valid + base + s) : 0u;
+            }
+            if (++cur_i == cur_n) {
+                cur_p = __shfl_sync(0xffffffffu, claim, 0);
+                if (cur_p < a.n_pieces) start_piece();
+            }
+            return true;
+        };
+        Job f0{}, f1{};
+        bool h0 = fetch(f0);
+        bool h1 = h0 && fetch(f1);
+        uint32_t stage = 0, phase = 0, nissued = 0;
+        while (h0) {
+            mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
+            StageMeta& mt = sh.meta[stage];
+            const uint32_t kdst = smem_base + stage * 2 * TB;
+            const uint32_t full = smem_u32(&sh.full[stage]);
+            uint32_t bytes = 0, invalid = 0;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const uint32_t s = k * 32 + lane;
+                if (s < NS) mt.valid[s] = uint8_t(f0.vl[k]);
+                bytes += __reduce_add_sync(0xffffffffu, f0.vl[k] ? 2 * P * D * 2 : 0u);
+                invalid |= __ballot_sync(0xffffffffu, s < NS && f0.vl[k] < P);
+            }
+            if (lane == 0) {
+                mt.unit = f0.u;
+                mt.piece = f0.p;
+                mt.chunk = f0.c | (invalid ? 0x80000000u : 0u);
+                // the unit's G query rows ride along (units are b-major: the q row block
+                // of unit u = b*H + h starts at u * G * D)
+                mbar_expect_tx(full, bytes + L.G * D * 2);
+                bulk_g2s(smem_u32(mt.q), q + size_t(f0.u) * L.G * D, L.G * D * 2, full);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+                const uint32_t s = k * 32 + lane;
+                if (s < NS && f0.vl[k]) {
+                    const size_t off = size_t(f0.gp[k]) * P * D;  // gp = head * pool_pages + page
+                    bulk_g2s(kdst + s * slot_stride, L.k_pool + off, P * D * 2, full);
+                    bulk_g2s(kdst + TB + s * slot_stride, L.v_pool + off, P * D * 2, full);
+                }
+            }
+            if (lane == 0) ATTN_TRACE(1 + (nissued & 63));  // producer issued chunk
+            ++nissued;
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
+            }
+            f0 = f1;
+            h0 = h1;
+            if (h1) h1 = fetch(f1);
+        }
+        // sentinel: no more chunks for this CTA
+        mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
+        if (lane == 0) {
+            sh.meta[stage].unit = 0xffffffffu;
+            mbar_arrive(smem_u32(&sh.full[stage]));
+        }
+        return;
+    }
+
+    // ============================== consumers =================================
+    const uint32_t g = lane >> 2, t4 = lane & 3;
+    const uint32_t G = L.G;
+    const float scale_log2 = rsqrtf(float(D)) * 1.4426950408889634f;
+    const uint32_t ns_log = 31 - __clz(NS);  // NS = 128 / P is a power of two
+    // logical row i of a chunk -> byte offset inside a tile
+    auto row_off = [&](uint32_t i) -> uint32_t {
+        return (i & (NS - 1)) * slot_stride + (i >> ns_log) * (D * 2);
+    };
+    const uint32_t row0 = warp * kWarpRows;
+    // per-thread smem offsets, identical for every chunk:
+    //   QK  A = K rows (ldmatrix): lanes 0-15 rows 0-15 at k-chunk 0, lanes 16-31 at chunk 1
+    //   PV  A = V^T (ldmatrix.trans): lanes 0-7 rows 0-7 ch 0, 8-15 rows 0-7 ch 8,
+    //       16-23 rows 8-15 ch 0, 24-31 rows 8-15 ch 8
+    const uint32_t qk_off = row_off(row0 + (lane & 7) + ((lane >> 3) & 1) * 8) + (lane >> 4) * 16;
+    const uint32_t pv_off = row_off(row0 + (lane & 7) + ((lane >> 4) & 1) * 8) + ((lane >> 3) & 1) * 16;
+    uint32_t rv_slot[2], rv_row[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t row = row0 + g + hh * 8;
+        rv_slot[hh] = row & (NS - 1);
+        rv_row[hh] = row >> ns_log;
+    }
+    uint16_t* pt0 = sh.p[warp][0];
+    uint16_t* pt1 = sh.p[warp][1];
+
+    uint32_t cur_u = 0xffffffffu, cur_p = 0xffffffffu, q_u = 0xffffffffu, seg_first = 0, seg_last = 0;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
+    float o[MT][4];
+    uint32_t qb[D / 16][2];
+
+    // Partial slot of (unit, piece within the unit, warp): the CTA that claims a piece
+    // processes all of its chunks, and every warp writes exactly one partial for it.
+    auto slot_of = [&](uint32_t unit, uint32_t piece, uint32_t wp) -> size_t {
+        return (size_t(unit) * a.max_pieces + piece) * kWarps + wp;
+    };
+
+    // LSE merge of every partial of unit mu for query head h into `out` (one warp).
+    // Every slot of the unit's runs is written each step, so the o rows are loaded
+    // without waiting for (m, l): lanes own D/32 contiguous channels, windows of 32
+    // slots, o loads 8 slots at a time, all independent — about one L2 round trip.
+    auto merge = [&](uint32_t mu, uint32_t h) {
+        constexpr int PER = D / 32;
+        const uint32_t nslots = (__ldg(a.unit_piece + mu) >> 16) * kWarps;
+        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16 + h * 2;
+        const float* pou = part_o + (slot_of(mu, 0, 0) * 8 + h) * D + lane * PER;
+        float acc[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
+        float lpart = 0.0f, M = -INFINITY;
+        for (uint32_t base = 0; base < nslots; base += 32) {
+            const uint32_t n = min(32u, nslots - base);
+            const float mv = lane < n ? __ldcg(mlu + (base + lane) * 16) : -INFINITY;
+            const float lv = lane < n ? __ldcg(mlu + (base + lane) * 16 + 1) : 0.0f;
+            float Mw = mv;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, off));
+            const float Mn = fmaxf(M, Mw);
+            if (Mn == -INFINITY) continue;  // nothing live so far (warp-uniform)
+            const float r = M == -INFINITY ? 0.0f : exp2f(M - Mn);
+            lpart *= r;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) acc[i] *= r;
+            M = Mn;
+            const float wl = mv == -INFINITY ? 0.0f : exp2f(mv - M);  // weight of slot base + lane
+            lpart += wl * lv;
+            for (uint32_t s0 = 0; s0 < n; s0 += 8) {
+                float v[8][PER];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float* src = pou + size_t(base + s0 + j) * 8 * D;
+                    if (s0 + j < n) {
+                        if (PER == 4) {
+                            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+                            v[j][0] = t.x; v[j][1] = t.y; v[j][2 % PER] = t.z; v[j][3 % PER] = t.w;
+                        } else {
+                            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+                            v[j][0] = t.x; v[j][1 % PER] = t.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < PER; ++i) v[j][i] = 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float wj = __shfl_sync(0xffffffffu, wl, (s0 + j) & 31);
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) acc[i] += wj * v[j][i];
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, off);
+        const float inv = 1.0f / lpart;
+        float* dst = out + (size_t(mu) * G + h) * D + lane * PER;  // out is [b][h*G + g][d], u = b*H + h
+        if (PER == 4)
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[0] * inv, acc[1 % PER] * inv, acc[2 % PER] * inv,
+                                                          acc[3 % PER] * inv);
+        else
+            *reinterpret_cast<float2*>(dst) = make_float2(acc[0] * inv, acc[1 % PER] * inv);
+        if (h == 0 && lane == 0) {  // every producer is past this unit: re-arm its flags
+            if (a.ready) a.ready[mu] = 0u;
+            if (a.scored) a.scored[mu] = 0u;
+        }
+    };
+
+    // Count this warp's chunks of its previous piece (prev_u); the warp that completes
+    // a unit queues its merge, done by the CTA's warps after the chunk loop.
+    if (warp == kWarps + 1) {
+        // ========================== bookkeeping warp ==============================
+        // Per piece flush: publish the consumers' partial stores (they are ordered
+        // before this warp by the flush barrier), count the piece's chunks, and if it
+        // completes its unit, run the unit's LSE merges — all off the streaming path
+        // (a gpu-scope fence under full HBM load costs microseconds).
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t fs = k % kFlushSlots;
+            mbar_wait(smem_u32(&sh.flush_full[fs]), (k / kFlushSlots) & 1);
+            const uint32_t u = sh.flush_unit[fs], chunks = sh.flush_chunks[fs];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&sh.flush_empty[fs]));
+            if (u == 0xffffffffu) break;  // the consumers are done
+            uint32_t complete = 0;
+            if (lane == 0) {
+                __threadfence();
+                const uint32_t nch = __ldg(a.chunk_base + u + 1) - __ldg(a.chunk_base + u);
+                const uint32_t c = chunks * kWarps;
+                if (atomicAdd(a.unit_done + u, c) + c == kWarps * nch) {
+                    __threadfence();  // acquire: every CTA's partials of u are visible
+                    a.unit_done[u] = 0u;  // re-arm for the next step
+                    complete = 1u;
+                }
+            }
+            if (__shfl_sync(0xffffffffu, complete, 0))
+                for (uint32_t h = 0; h < G; ++h) merge(u, h);
+        }
+        if (lane == 0) ATTN_TRACE(242);  // bookkeeping done (merges included)
+        // the last CTA out re-arms the claim counter for the next step (every claim of
+        // this CTA precedes the consumers' final flush)
+        if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(a.work + 1, 1u) == a.ncta - 1) {
+                a.work[0] = 0u;
+                a.work[1] = 0u;
+            }
+        }
+        return;
+    }
+
+    uint32_t nflush = 0;  // piece flushes so far (identical sequence in every consumer warp)
+    // hand a flush (piece unit, chunks; unit = 0xffffffff ends) to the bookkeeping warp
+    auto signal_flush = [&](uint32_t k, uint32_t unit, uint32_t chunks) {
+        const uint32_t fs = k % kFlushSlots;
+        __syncwarp();
+        if (lane == 0) {
+            if (warp == 0) {
+                if (k >= uint32_t(kFlushSlots))
+                    mbar_wait(smem_u32(&sh.flush_empty[fs]), ((k / kFlushSlots) - 1) & 1);
+                sh.flush_unit[fs] = unit;
+                sh.flush_chunks[fs] = chunks;
+            }
+            mbar_arrive(smem_u32(&sh.flush_full[fs]));  // release: this warp's partial stores
+        }
+    };
+
+    // Emit this warp's partial of piece cur_p (unit cur_u, chunks seg_first..seg_last)
+    // and hand the piece to the bookkeeping warp; no barrier with the other warps.
+    auto flush = [&]() {
+        float lsum[2] = {l_run[0], l_run[1]};
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc)
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
+        const size_t slot = slot_of(cur_u, cur_p - (__ldg(a.unit_piece + cur_u) & 0xffffu), warp);
+        float* po = part_o + slot * 8 * D;
+        float* ml = part_ml + slot * 16;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const uint32_t c0 = m * 16 + g;
+#pragma unroll
+            for (int hc = 0; hc < 2; ++hc) {
+                const uint32_t h = 2 * t4 + hc;
+                if (h < G) {
+                    po[h * D + c0] = o[m][hc];
+                    po[h * D + c0 + 8] = o[m][2 + hc];
+                }
+            }
+        }
+        if (g == 0) {  // m and l are warp-uniform per head
+            ml[(2 * t4) * 2] = m_run[0];
+            ml[(2 * t4) * 2 + 1] = lsum[0];
+            ml[(2 * t4 + 1) * 2] = m_run[1];
+            ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
+        }
+        signal_flush(nflush++, cur_u, seg_last - seg_first + 1);
+    };
+
+    uint32_t stage = 0, phase = 0, nchunk = 0;
+    for (;; ++nchunk) {
+        mbar_wait(smem_u32(&sh.full[stage]), phase);
+        if (tid == 0) ATTN_TRACE(64 + (nchunk & 63));  // data arrived (warp 0)
+        const StageMeta& mt = sh.meta[stage];
+        const uint32_t u = mt.unit;
+        if (u == 0xffffffffu) break;  // the producer has no more chunks
+        const uint32_t chunk = mt.chunk & 0x7fffffffu;
+        const bool new_piece = mt.piece != cur_p;
+        const uint32_t k_base = smem_base + stage * 2 * TB;
+        const uint32_t v_base = k_base + TB;
+        const bool any_invalid = (mt.chunk >> 31) != 0;
+        if (any_invalid) {
+            // zero this warp's V rows that carry no token: stale or uninitialised smem
+            // could hold NaN/Inf, and 0 * NaN would poison the PV product
+            for (uint32_t e = lane; e < kWarpRows * (D / 8); e += 32) {
+                const uint32_t row = row0 + e / (D / 8), ch = e % (D / 8);
+                if ((row >> ns_log) >= mt.valid[row & (NS - 1)]) {
+                    unsigned char* p = smem + stage * 2 * TB + TB + row_off(row) + ch * 16;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+                }
+            }
+            __syncwarp();
+        }
+
+        // On a unit change the new unit's Q^T fragments (B operand) come from the q rows
+        // staged with the chunk: b0 = Q[g][16ks+2t..], b1 = Q[g][16ks+8+2t..]. The old
+        // unit's flush below needs only o / m / l, so qb can be replaced right away.
+        if (u != q_u) {
+            q_u = u;
+            const uint16_t* qrow = mt.q + g * D;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                qb[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 2 * t4) : 0u;
+                qb[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + ks * 16 + 8 + 2 * t4) : 0u;
+            }
+        }
+        // S^T = K Q^T over the warp's 16 rows straight from the stage (two accumulator
+        // chains, even / odd ks); then the V fragments go to registers and the stage is
+        // released: softmax, PV and any flush of the previous unit run on registers
+        // while the producer refills it, so a stage is held only for QK + ldmatrix.
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(k_base + qk_off + ks * 32, a0, a1, a2, a3);
+            mma_bf16((ks & 1) ? s2 : s, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+        }
+        uint32_t vf[MT][4];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) ldsm_x4_t(v_base + pv_off + m * 32, vf[m][0], vf[m][1], vf[m][2], vf[m][3]);
+        bool rv[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) rv[hh] = !any_invalid || rv_row[hh] < mt.valid[rv_slot[hh]];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i] += s2[i];
+        // the fragments must have left shared memory before the stage is released:
+        // empty asms consuming S and every V fragment register make the warp wait
+        asm volatile("" ::"f"(s[0]), "f"(s[1]), "f"(s[2]), "f"(s[3]) : "memory");
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+            asm volatile("" ::"r"(vf[m][0]), "r"(vf[m][1]), "r"(vf[m][2]), "r"(vf[m][3]) : "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sh.empty[stage]));
+        if (tid == 0) ATTN_TRACE(128 + (nchunk & 63));  // stage released (warp 0)
+
+        if (new_piece) {
+            if (tid == 0) ATTN_TRACE(192 + 2 * (nflush & 3));
+            if (cur_u != 0xffffffffu) flush();
+            if (tid == 0) ATTN_TRACE(193 + 2 * (nflush & 3));
+            cur_u = u;
+            cur_p = mt.piece;
+            seg_first = chunk;
+            m_run[0] = m_run[1] = -INFINITY;
+            l_run[0] = l_run[1] = 0.0f;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.0f;
+        }
+        seg_last = chunk;
+
+        // warp-local online softmax: this warp is its own split
+        float mnew[2];
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            float mx = fmaxf(rv[0] ? s[hc] : -INFINITY, rv[1] ? s[2 + hc] : -INFINITY);
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            mnew[hc] = fmaxf(m_run[hc], mx * scale_log2);
+            const float alpha = mnew[hc] == -INFINITY ? 1.0f : exp2f(m_run[hc] - mnew[hc]);
+            m_run[hc] = mnew[hc];
+            l_run[hc] *= alpha;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                o[m][hc] *= alpha;
+                o[m][2 + hc] *= alpha;
+            }
+        }
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            const float p0 = rv[0] ? exp2f(fmaf(s[hc], scale_log2, -mnew[hc])) : 0.0f;
+            const float p1 = rv[1] ? exp2f(fmaf(s[2 + hc], scale_log2, -mnew[hc])) : 0.0f;
+            l_run[hc] += p0 + p1;
+            const int h = 2 * t4 + hc;
+            const uint16_t h0 = f2bf(p0), h1 = f2bf(p1);
+            pt0[h * kPStride + g] = h0;
+            pt0[h * kPStride + g + 8] = h1;
+            pt1[h * kPStride + g] = f2bf(p0 - __uint_as_float(uint32_t(h0) << 16));
+            pt1[h * kPStride + g + 8] = f2bf(p1 - __uint_as_float(uint32_t(h1) << 16));
+        }
+        __syncwarp();
+        // O^T += V^T P^T, K = the warp's 16 rows: b0 = P[head g][rows 2t..], b1 = rows 8+2t..
+        const uint32_t b00 = *reinterpret_cast<const uint32_t*>(pt0 + g * kPStride + 2 * t4);
+        const uint32_t b01 = *reinterpret_cast<const uint32_t*>(pt0 + g * kPStride + 8 + 2 * t4);
+        const uint32_t b10 = *reinterpret_cast<const uint32_t*>(pt1 + g * kPStride + 2 * t4);
+        const uint32_t b11 = *reinterpret_cast<const uint32_t*>(pt1 + g * kPStride + 8 + 2 * t4);
+        __syncwarp();  // P tile reads done before the next chunk overwrites it
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            mma_bf16(o[m], vf[m][0], vf[m][1], vf[m][2], vf[m][3], b00, b01);
+            mma_bf16(o[m], vf[m][0], vf[m][1], vf[m][2], vf[m][3], b10, b11);
+        }
+        if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
+    if (tid == 0) ATTN_TRACE(240);
+    if (cur_u != 0xffffffffu) flush();
+    signal_flush(nflush, 0xffffffffu, 0u);
+    if (tid == 0) ATTN_TRACE(241);
+}
+
+__host__ __device__ constexpr size_t attn_smem_bytes(uint32_t D, uint32_t P) {
+    return size_t(kStages) * 2 * tile_bytes(D, P) + (D == 64 ? sizeof(SmemHead<64>) : sizeof(SmemHead<128>));
+}
+
+}  // namespace attn
+}  // namespace absp
