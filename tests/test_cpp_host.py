@@ -38,6 +38,6 @@ def test_cpp_host_layer_cpu(tmp_path):
 @pytest.mark.gpu
 def test_cpp_host_layer_gpu(tmp_path):
     exe = _compile(tmp_path)
-    r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr + r.stdout
     assert "OK gpu" in r.stdout
