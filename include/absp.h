@@ -176,6 +176,12 @@ absp_status absp_last_selection(absp_ctx* ctx, uint32_t layer, const uint32_t** 
 
 absp_status absp_get_layer_info(absp_ctx* ctx, uint32_t layer, absp_layer_info* info);
 
+/* The last selection of `layer` (absp_decode_step's or absp_select's context-owned
+ * buffers) copied to HOST memory in SelectionResult::blocks order (engine.hpp:19-26):
+ * blocks uint32 [batch][num_kv_heads][blocks_stride] (blocks_stride from
+ * absp_last_selection), counts uint32 [batch][num_kv_heads]. Synchronous. */
+absp_status absp_download_selection(absp_ctx* ctx, uint32_t layer, uint32_t* blocks, uint32_t* counts);
+
 /* Read back one sequence's store in the reference layouts (synchronous):
  *   offsets           : uint64 [H+1]       (CentroidStore::offsets)
  *   values/values_min : fp32 [total][d]    (CentroidStore::values / values_min;
@@ -192,6 +198,13 @@ absp_status absp_download_store(absp_ctx* ctx, uint32_t layer, uint32_t seq, uin
 /* Scores of the last absp_select/absp_decode_step for one sequence, flattened
  * like estimate_scores' output (fp32 [total]); synchronous. */
 absp_status absp_download_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* scores);
+
+/* Diagnostics of absp_decode_step's selection filter (INT4 mean stores, select.cu):
+ * the approximate scores of one sequence (fp32 [total], estimate_scores layout) and
+ * the per-KV-head error bound E_h with |approx - exact| <= E_h; synchronous. Only
+ * meaningful after a decode step that used the filter. */
+absp_status absp_download_filter_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* approx,
+                                        float* err);
 
 /* Deterministic counter-based N(0,1)-like bf16 generator used by the benchmark
  * and tests (same bytes as oracle/synth.py): element i of stream s gets

@@ -320,6 +320,23 @@ class DecodeAttention {
                                   p(s.zero_points_min)));
         return s;
     }
+    // The layer's last selection (decode_step / select) per (sequence, KV head).
+    Selection download_selection(uint32_t layer) const {
+        const uint32_t* b = nullptr;
+        const uint32_t* c = nullptr;
+        uint32_t stride = 0;
+        check(absp_last_selection(ctx_, layer, &b, &stride, &c));
+        const absp_layer_info info = layer_info(layer);
+        const std::size_t H = config_.num_heads, units = std::size_t(info.batch) * H;
+        std::vector<uint32_t> blocks(units * stride), counts(units);
+        check(absp_download_selection(ctx_, layer, blocks.data(), counts.data()));
+        Selection s;
+        s.batch = info.batch;
+        s.num_heads = H;
+        for (std::size_t u = 0; u < units; ++u)
+            s.blocks.emplace_back(blocks.begin() + u * stride, blocks.begin() + u * stride + counts[u]);
+        return s;
+    }
     // estimate_scores' flattened output for one sequence (engine.hpp:47-49).
     std::vector<float> download_scores(uint32_t layer, uint32_t seq) const {
         std::vector<uint64_t> off(config_.num_heads + 1);

@@ -11,7 +11,7 @@
  *
  * Every function cites the reference code it restates. Parity is pinned by
  * tests/test_oracle_*.py against (a) the reference's own known-answer tests
- * (proj/tests/*.cpp), re-expressed, and (b) the unmodified reference core
+ * (proj/tests/*\.cpp), re-expressed, and (b) the unmodified reference core
  * compiled into oracle/_ref/ (see oracle/Makefile) on the same inputs, plus the
  * committed fixtures in tests/golden/.
  *

@@ -303,6 +303,28 @@ class DecodeAttention:
         check(self._lib.absp_last_selection(self._ctx, layer, C.byref(b), C.byref(s), C.byref(c)))
         return b.value, s.value, c.value
 
+    def download_selection(self, layer: int) -> list:
+        """The layer's last selection (decode_step or select) as [batch][kv head] arrays of
+        block ids, score-descending (SelectionResult::blocks, engine.hpp:19-26)."""
+        _, stride, _ = self.last_selection(layer)
+        batch = len(self._seq_lens[layer])
+        H = self.config.num_heads
+        blocks = np.zeros((batch, H, stride), np.uint32)
+        counts = np.zeros((batch, H), np.uint32)
+        check(self._lib.absp_download_selection(self._ctx, layer, blocks.ctypes.data, counts.ctypes.data))
+        return [[blocks[b, h, :counts[b, h]].copy() for h in range(H)] for b in range(batch)]
+
+    def download_filter_scores(self, layer: int, seq: int):
+        """(approximate scores [total], per-KV-head error bounds [H]) of the decode step's
+        selection filter for one sequence (diagnostics)."""
+        offsets = np.zeros(self.config.num_heads + 1, np.uint64)
+        check(self._lib.absp_download_store(self._ctx, layer, seq, offsets.ctypes.data,
+                                            None, None, None, None, None, None, None, None))
+        approx = np.zeros(int(offsets[-1]), np.float32)
+        err = np.zeros(self.config.num_heads, np.float32)
+        check(self._lib.absp_download_filter_scores(self._ctx, layer, seq, approx.ctypes.data, err.ctypes.data))
+        return approx, err
+
     def launch_count(self) -> int:
         return int(self._lib.absp_launch_count(self._ctx))
 

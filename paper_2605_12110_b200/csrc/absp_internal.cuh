@@ -138,6 +138,13 @@ cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList&
                           float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches);
 size_t attend_smem_bytes(uint32_t D, uint32_t P);
+// Decode-step selection via tensor-core filter + exact refine (select.cu): same
+// ordered selections as launch_score + launch_topk, without full exact scores.
+bool select_fast_supported(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget);
+cudaError_t init_select_attributes();  // per device, once
+cudaError_t launch_select_fast(const LayerView& L, const uint16_t* q, const ScoreWork& work, float* approx,
+                               float* err, uint32_t* blocks, uint32_t stride, uint32_t* counts,
+                               const PageList& pages, cudaStream_t s, int* launches);
 cudaError_t init_attend_attributes();  // per device, once
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -115,6 +116,7 @@ struct Layer {
     DevBuf<float> values, values_min, scales, zps, scales_min, zps_min, scores;
     DevBuf<uint32_t> codes, codes_min;
     DevBuf<uint32_t> sel_blocks, sel_counts;
+    DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
     DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
     DevBuf<float> stage_out;
@@ -125,6 +127,7 @@ struct Layer {
         scales_min.release(); zps_min.release(); scores.release();
         codes.release(); codes_min.release();
         sel_blocks.release(); sel_counts.release();
+        approx.release(); unit_err.release();
         part_o.release(); part_ml.release();
         stage_q.release(); stage_out.release();
         step_work.release();
@@ -138,6 +141,7 @@ struct Layer {
 struct absp_ctx {
     int device = 0;
     int num_sms = 148;
+    bool fast_select = false;  // ABSP_FAST_SELECT=1: decode steps select through select.cu
     absp_config cfg{};
     std::vector<Layer> layers;
     uint64_t launches = 0;
@@ -337,9 +341,12 @@ absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) 
                                     std::to_string(prop.major) + std::to_string(prop.minor));
     ABSP_CUDA(init_attend_attributes());
     ABSP_CUDA(init_score_attributes());
+    ABSP_CUDA(init_select_attributes());
     auto* ctx = new absp_ctx;
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
+    const char* fs = std::getenv("ABSP_FAST_SELECT");
+    ctx->fast_select = fs && fs[0] == '1';
     ctx->cfg = *cfg;
     ctx->layers.resize(cfg->num_layers);
     *out = ctx;
@@ -490,6 +497,8 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
         }
     }
     ABSP_CUDA(l->scores.ensure(l->total_cap));
+    ABSP_CUDA(l->approx.ensure(l->total_cap));
+    ABSP_CUDA(l->unit_err.ensure(units));
     l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
     ABSP_CUDA(l->sel_counts.ensure(units));
@@ -612,8 +621,19 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     if (!q || !out) return fail(ABSP_EINVAL, "decode_step: null pointer");
     DeviceGuard dg(ctx->device);
     const cudaStream_t s = cudaStream_t(stream);
-    st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, s);
-    if (st != ABSP_OK) return st;
+    const LayerView v = view_of(ctx, *l);
+    if (ctx->fast_select && select_fast_supported(v, l->max_nblocks, l->max_budget)) {
+        const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1)};
+        int n = 0;
+        cudaError_t e = launch_select_fast(v, static_cast<const uint16_t*>(q), sw, l->approx.p, l->unit_err.p,
+                                           l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->step_work.pages(), s,
+                                           &n);
+        ctx->launches += n;
+        if (e != cudaSuccess) return cuda_fail(e, "select kernels");
+    } else {
+        st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, s);
+        if (st != ABSP_OK) return st;
+    }
     l->selected = true;
     return do_attend_step(ctx, l, q, out, s);
 }
@@ -732,6 +752,41 @@ absp_status absp_download_store(absp_ctx* ctx, uint32_t layer, uint32_t seq, uin
     return ABSP_OK;
 }
 
+absp_status absp_download_selection(absp_ctx* ctx, uint32_t layer, uint32_t* blocks, uint32_t* counts) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->bound) return fail(ABSP_ESTATE, "download_selection: layer not bound");
+    if (!blocks || !counts) return fail(ABSP_EINVAL, "download_selection: null pointer");
+    DeviceGuard dg(ctx->device);
+    ABSP_CUDA(cudaDeviceSynchronize());
+    const size_t units = l->desc.size();
+    ABSP_CUDA(cudaMemcpy(blocks, l->sel_blocks.p, units * l->sel_stride * 4, cudaMemcpyDeviceToHost));
+    ABSP_CUDA(cudaMemcpy(counts, l->sel_counts.p, units * 4, cudaMemcpyDeviceToHost));
+    return ABSP_OK;
+}
+
+absp_status absp_download_filter_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* approx,
+                                        float* err) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "download_filter_scores: store not built");
+    if (seq >= l->batch) return fail(ABSP_ERANGE, "download_filter_scores: sequence out of range");
+    if (!approx || !err) return fail(ABSP_EINVAL, "null pointer");
+    DeviceGuard dg(ctx->device);
+    ABSP_CUDA(cudaDeviceSynchronize());
+    const uint32_t H = ctx->cfg.num_kv_heads;
+    uint64_t off = 0;
+    for (uint32_t h = 0; h < H; ++h) {
+        const UnitDesc& d = l->desc[size_t(seq) * H + h];
+        ABSP_CUDA(cudaMemcpy(approx + off, l->approx.p + d.seg, size_t(d.n_blocks) * 4, cudaMemcpyDeviceToHost));
+        ABSP_CUDA(cudaMemcpy(err + h, l->unit_err.p + size_t(seq) * H + h, 4, cudaMemcpyDeviceToHost));
+        off += d.n_blocks;
+    }
+    return ABSP_OK;
+}
+
 absp_status absp_download_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* scores) {
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
@@ -771,6 +826,11 @@ namespace absp {
 cudaError_t debug_attn_trace(void* dst, size_t bytes);
 cudaError_t debug_score_trace(void* dst, size_t bytes);
 cudaError_t debug_topk_trace(void* dst, size_t bytes);
+cudaError_t debug_refine_trace(void* dst, size_t bytes, void* cand, size_t cbytes);
+}
+extern "C" absp_status absp_debug_refine_trace(void* dst, size_t bytes, void* cand, size_t cbytes) {
+    cudaError_t e = absp::debug_refine_trace(dst, bytes, cand, cbytes);
+    return e == cudaSuccess ? ABSP_OK : cuda_fail(e, "debug_refine_trace");
 }
 extern "C" absp_status absp_debug_topk_trace(void* dst, size_t bytes) {
     cudaError_t e = absp::debug_topk_trace(dst, bytes);

@@ -17,6 +17,7 @@
 // Appendix A).
 #include "absp_internal.cuh"
 #include "ptx.cuh"
+#include "common.cuh"
 
 namespace absp {
 namespace {
@@ -38,10 +39,6 @@ __device__ __forceinline__ void score_trace(int slot) {
 #define SCORE_TRACE(slot) do {} while (0)
 #endif
 
-__device__ __forceinline__ float bf16f(uint16_t x) { return __uint_as_float(uint32_t(x) << 16); }
-
-__device__ __forceinline__ float ref_max(float a, float b) { return (a < b) ? b : a; }
-
 // Group-summed query for unit (b, h) into smem.
 template <int D>
 __device__ __forceinline__ void load_query(const LayerView& L, const UnitDesc& du,
@@ -53,24 +50,6 @@ __device__ __forceinline__ void load_query(const LayerView& L, const UnitDesc& d
         qs[c] = acc;
     }
 }
-
-// Byte offset (code * 4) of nibble/crumb k of a packed code word, for a 4-byte
-// table entry. 4-bit: two masked copies hold the even / odd nibbles pre-scaled by 4
-// in their bytes, and one PRMT per code extracts a byte (1.5 ALU ops per code).
-template <int BITS>
-struct CodeOffsets {
-    uint32_t a, b, w;
-    __device__ __forceinline__ explicit CodeOffsets(uint32_t word) : w(word) {
-        if (BITS == 4) {
-            a = (word << 2) & 0x3c3c3c3cu;  // nibbles 0,2,4,6 (x4) in bytes 0..3
-            b = (word >> 2) & 0x3c3c3c3cu;  // nibbles 1,3,5,7 (x4)
-        }
-    }
-    __device__ __forceinline__ uint32_t operator()(int k) const {
-        if (BITS == 4) return __byte_perm((k & 1) ? b : a, 0u, 0x4440u | uint32_t(k >> 1));
-        return ((w >> (k * BITS)) & ((1u << BITS) - 1u)) << 2;
-    }
-};
 
 // Table path (bits in {2, 4}; MAXMIN doubles the tables and code streams).
 //

@@ -26,6 +26,7 @@
 //      producer: page id and valid-row count per page slot.
 #include "absp_internal.cuh"
 #include "ptx.cuh"
+#include "common.cuh"
 
 namespace absp {
 namespace {
@@ -50,11 +51,6 @@ __device__ __forceinline__ void topk_trace(int slot) {
 #define TOPK_TRACE(slot) do {} while (0)
 #endif
 
-__device__ __forceinline__ uint32_t order_key(float f) {
-    uint32_t u = __float_as_uint(f);
-    if ((u & 0x7fffffffu) == 0u) u = 0u;  // -0.0 == +0.0
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 struct TopkSmem {
     uint32_t hist[kWarps][32];
@@ -92,40 +88,6 @@ __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t pr
     for (int b = 0; b < 5; ++b)
         if (b < nbits) mm &= __ballot_sync(0xffffffffu, (key >> (shift + b)) & 1u) ^ xm[b];
     return __popc(mm);
-}
-
-// Resolve the ordered selection `out` of unit u to pool pages for the attention
-// producer (the reference's populate_page_spans, engine.cpp:271-283): slot
-// s = entry * (B/P) + page; slots up to the end of the unit's last 128-row
-// attention chunk are written, empty ones with valid = 0. Block sizes and P are
-// powers of two (checked by absp_config_validate), so no divisions.
-__device__ __forceinline__ void resolve_pages(const LayerView& L, const UnitDesc& du, uint32_t u,
-                                              uint32_t sel_total, const uint32_t* out,
-                                              const PageList& pages) {
-    if (!pages.page) return;
-    const uint32_t ppb_log = __ffs(du.block) - __ffs(L.P);  // log2(B / P)
-    const uint32_t p_log = __ffs(L.P) - 1;
-    const uint32_t E = kAttnChunkRows / du.block;
-    const uint32_t slot_end = ((sel_total + E - 1) / E * E) << ppb_log;
-    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
-    const uint32_t head_base = du.head * uint32_t(L.pool_pages);
-    const size_t base = size_t(pages.chunk_base[u]) * pages.ns;
-    uint32_t* pg = pages.page + base;
-    uint16_t* vl = pages.valid + base;
-    __syncthreads();  // `out` (global) written by this block is visible block-wide
-    for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
-        const uint32_t e = s >> ppb_log, pp = s & ((1u << ppb_log) - 1u);
-        uint32_t v = 0, page = 0;
-        if (e < sel_total) {
-            const uint32_t t0 = out[e] * du.block + (pp << p_log);
-            if (t0 < du.n_tokens) {
-                v = min(L.P, du.n_tokens - t0);
-                page = head_base + __ldg(pt + (t0 >> p_log));
-            }
-        }
-        pg[s] = page;
-        vl[s] = uint16_t(v);
-    }
 }
 
 template <bool REG, int ITEMS>

@@ -162,6 +162,16 @@ void gpu_tests() {
     da.bind(0, k, v, pool_pages, pt, max_pages, lens);
     EXPECT(throws<std::logic_error>([&] { da.decode_step(0, q, out); }));  // store not built
     da.build_store(0);
+    // absp_select fills the reference's full estimate_scores output (checked below);
+    // absp_decode_step selects through its own path and must pick the same blocks
+    const absp_layer_info info = da.layer_info(0);
+    uint32_t *sblocks = nullptr, *scounts = nullptr;
+    cuda_ok(cudaMalloc(&sblocks, batch * H * info.max_select * 4), "malloc sblocks");
+    cuda_ok(cudaMalloc(&scounts, batch * H * 4), "malloc scounts");
+    da.select(0, q, sblocks, info.max_select, scounts);
+    cuda_ok(cudaDeviceSynchronize(), "select");
+    std::vector<std::vector<float>> exact_scores;
+    for (uint32_t b = 0; b < batch; ++b) exact_scores.push_back(da.download_scores(0, b));
     da.decode_step(0, q, out);
     cuda_ok(cudaDeviceSynchronize(), "decode_step");
 
@@ -214,7 +224,7 @@ void gpu_tests() {
         EXPECT(st.codes == codes);
         EXPECT(std::memcmp(st.scales.data(), scales.data(), scales.size() * 4) == 0);
         EXPECT(std::memcmp(st.zero_points.data(), zps.data(), zps.size() * 4) == 0);
-        const std::vector<float> dsc = da.download_scores(0, b);
+        const std::vector<float>& dsc = exact_scores[b];
         EXPECT(dsc.size() == scores.size() && std::memcmp(dsc.data(), scores.data(), scores.size() * 4) == 0);
         for (std::size_t h = 0; h < H; ++h) {
             EXPECT(dcounts[b * H + h] == wcounts[h]);
@@ -239,6 +249,8 @@ void gpu_tests() {
     }
     std::printf("max attention error %.3g, %llu kernel launches\n", max_err,
                 (unsigned long long)da.launch_count());
+    cudaFree(sblocks);
+    cudaFree(scounts);
     cudaFree(k);
     cudaFree(v);
     cudaFree(q);

@@ -1,6 +1,8 @@
 """Runs a host-side Layer (tests/layer_data.py) through the C ABI on cuda:0."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -17,7 +19,8 @@ def to_dev_u32(a: np.ndarray) -> torch.Tensor:
 
 
 class GpuLayer:
-    def __init__(self, layer, T, method=0, bits=4, mode=1, max_seq_len=None, candidates=None):
+    def __init__(self, layer, T, method=0, bits=4, mode=1, max_seq_len=None, candidates=None, fast=False):
+        """fast=True: decode steps select through select.cu (ABSP_FAST_SELECT=1)."""
         self.layer = layer
         cands = sorted(set(candidates or layer.block_sizes))
         self.cfg = EngineConfig(num_heads=layer.H, head_dim=layer.d, page_size=layer.P,
@@ -26,7 +29,15 @@ class GpuLayer:
                                 quant=QuantSpec(bits, QuantMode(mode)) if bits else None,
                                 num_q_heads=layer.H * layer.G, max_batch=layer.batch,
                                 max_seq_len=max_seq_len or max(layer.seq_lens), num_layers=1)
-        self.da = DecodeAttention(self.cfg)
+        old = os.environ.get("ABSP_FAST_SELECT")
+        os.environ["ABSP_FAST_SELECT"] = "1" if fast else "0"
+        try:
+            self.da = DecodeAttention(self.cfg)
+        finally:
+            if old is None:
+                del os.environ["ABSP_FAST_SELECT"]
+            else:
+                os.environ["ABSP_FAST_SELECT"] = old
         self.da.set_assignment(0, BlockAssignment(list(layer.block_sizes)))
         self.k = to_dev_u16(layer.k_pool)
         self.v = to_dev_u16(layer.v_pool)
@@ -67,6 +78,7 @@ class GpuLayer:
         out = torch.empty(L.batch, L.H * L.G, L.d, dtype=torch.float32, device="cuda")
         self.da.decode_step(0, self.q, out)
         torch.cuda.synchronize()
+        self.step_selection = self.da.download_selection(0)
         return out.cpu().numpy()
 
 

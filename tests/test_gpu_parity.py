@@ -63,6 +63,10 @@ def test_golden_cases(cuda, golden, name):
     assert np.array_equal(np.array([len(s) for s in sel], np.uint32), g("sel_counts"))
     assert np.array_equal(np.concatenate(sel), g("sel_blocks"))
     out = gl.decode()[0]
+    # the decode step selects through its own path (select.cu for int4 mean): same blocks
+    dsel = gl.step_selection[0]
+    assert np.array_equal(np.array([len(s) for s in dsel], np.uint32), g("sel_counts"))
+    assert np.array_equal(np.concatenate(dsel), g("sel_blocks"))
     ok, err = within_tol(out, g("attn_out"))
     assert ok, f"max abs err {err}"
     if c["n"] <= c["T"]:  # full coverage: also within tolerance of the fp64 oracle
@@ -91,6 +95,7 @@ def test_random_batches_vs_oracle(cuda, G, H, P, cands, seq_lens, T):
         assert np.array_equal(_bits(gl.da.download_scores(0, b)), _bits(sc))
         for h in range(H):
             assert np.array_equal(sel[b][h], want_sel[h]), (b, h)
+            assert np.array_equal(gl.step_selection[b][h], want_sel[h]), ("decode step", b, h)
         ok, err = within_tol(out[b], want)
         assert ok, f"seq {b}: max abs err {err}"
 
@@ -122,6 +127,60 @@ def test_ties_pick_lowest_indices(cuda):
         n_blocks = (4000 + b - 1) // b
         k = (256 + b - 1) // b
         assert sel[h].tolist() == list(range(k - 1)) + [n_blocks - 1]
+
+
+@pytest.mark.parametrize("n,T", [(70000, 256), (3000, 512)])
+def test_fast_select_ties(cuda, n, T):
+    """Constant keys: every score ties, so the decode step's filter keeps every block as a
+    candidate — past its capacity at n=70000 (B=16: 4375 blocks), which re-scores all
+    blocks exactly; ties go to the lowest block ids, the trailing block is forced in."""
+    from gpu_util import GpuLayer
+    layer = make_layer(5, H=2, G=2, d=128, P=16, block_sizes=(16, 32), seq_lens=(n,))
+    layer.k_pool[:] = 0x3F80
+    gl = GpuLayer(layer, T, fast=True)
+    gl.decode()
+    for h, b in enumerate(layer.block_sizes):
+        n_blocks = (n + b - 1) // b
+        k = (T + b - 1) // b
+        assert gl.step_selection[0][h].tolist() == list(range(k - 1)) + [n_blocks - 1]
+
+
+def test_filter_error_bound(cuda):
+    """select.cu's premise: |approx - exact| <= E per unit (with room to spare), so the
+    candidate set provably contains the exact top-K."""
+    from gpu_util import GpuLayer
+    for scale in (0.05, 1.0, 20.0):
+        layer = make_layer(11, H=8, G=4, d=128, P=16, seq_lens=(9000, 3000), scale=scale)
+        gl = GpuLayer(layer, 1024, fast=True)
+        gl.select()
+        exact = [gl.da.download_scores(0, b) for b in range(layer.batch)]
+        gl.decode()
+        for b in range(layer.batch):
+            approx, err = gl.da.download_filter_scores(0, b)
+            off = np.concatenate([[0], np.cumsum([(n + bs - 1) // bs for n, bs in
+                                                  zip([layer.seq_lens[b]] * layer.H, layer.block_sizes)])])
+            for h in range(layer.H):
+                a, e = approx[off[h]:off[h + 1]], exact[b][off[h]:off[h + 1]]
+                dev = np.abs(a.astype(np.float64) - e).max()
+                assert dev <= err[h] / 8, (scale, b, h, dev, err[h])
+                # the bound is meaningful: well below the spread of the scores
+                assert err[h] < 0.05 * (e.max() - e.min()), (scale, b, h, err[h])
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_decode_step_selection_many_seeds(cuda, fast):
+    """The decode step's selection (exact scorer + top-k, or select.cu's filter + exact
+    refine) against the oracle's exact top-K on many units with score distributions of
+    different widths (key scales 0.01 .. 10)."""
+    from gpu_util import GpuLayer
+    for seed, scale in enumerate((0.01, 0.3, 1.0, 10.0)):
+        layer = make_layer(100 + seed, H=8, G=4, d=128, P=16, seq_lens=(20000, 7777, 513), scale=scale)
+        gl = GpuLayer(layer, 2048, fast=fast)
+        gl.decode()
+        for b in range(layer.batch):
+            _, _, want_sel, _ = oracle_step(layer, b, 2048)
+            for h in range(layer.H):
+                assert np.array_equal(gl.step_selection[b][h], want_sel[h]), (scale, b, h)
 
 
 def test_block_to_pages_through_attend(cuda):
