@@ -120,6 +120,22 @@ struct Layer {
     DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
     DevBuf<float> stage_out;
+    // absp_decode_step_host as one CUDA graph: H2D q -> step kernels -> D2H out; the
+    // copy nodes are re-pointed when the caller's host buffers change
+    cudaGraph_t host_graph = nullptr;  // kept: the exec's copy nodes are addressed through it
+    cudaGraphExec_t host_exec = nullptr;
+    cudaGraphNode_t h2d_node = nullptr, d2h_node = nullptr;
+    const void* host_q = nullptr;
+    float* host_out = nullptr;
+    int host_launches = 0;
+    void drop_host_graph() {
+        if (host_exec) cudaGraphExecDestroy(host_exec);
+        if (host_graph) cudaGraphDestroy(host_graph);
+        host_exec = nullptr;
+        host_graph = nullptr;
+        host_q = nullptr;
+        host_out = nullptr;
+    }
 
     void release() {
         d_desc.release(); d_items.release(); d_item_begin.release();
@@ -130,6 +146,7 @@ struct Layer {
         approx.release(); unit_err.release();
         part_o.release(); part_ml.release();
         stage_q.release(); stage_out.release();
+        drop_host_graph();
         step_work.release();
         for (auto& kv : attend_work) kv.second.release();
         attend_work.clear();
@@ -382,6 +399,7 @@ absp_status absp_set_assignment(absp_ctx* ctx, uint32_t layer, const uint32_t* b
                                          std::to_string(b) + " is not a multiple of page_size");
     }
     l->block_sizes.assign(block_sizes, block_sizes + c.num_kv_heads);
+    l->drop_host_graph();
     l->assigned = true;
     l->bound = false;
     l->built = false;
@@ -419,6 +437,7 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
 
     DeviceGuard dg(ctx->device);
     if (!dg.ok) return fail(ABSP_ECUDA, "cudaSetDevice failed");
+    l->drop_host_graph();
     l->k_pool = static_cast<const uint16_t*>(k_pool);
     l->v_pool = static_cast<const uint16_t*>(v_pool);
     l->pool_pages = pool_pages;
@@ -638,6 +657,60 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     return do_attend_step(ctx, l, q, out, s);
 }
 
+// Captures H2D q -> absp_decode_step -> D2H out of `layer` into a graph (host
+// pointers as given; later calls re-point the copy nodes).
+static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, const void* q_host, float* out_host,
+                                     size_t nq) {
+    cudaStream_t cap = nullptr;
+    ABSP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    const uint64_t before = ctx->launches;
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    absp_status st = ABSP_OK;
+    if (e == cudaSuccess) {
+        e = cudaMemcpyAsync(l->stage_q.p, q_host, nq * sizeof(uint16_t), cudaMemcpyHostToDevice, cap);
+        if (e == cudaSuccess) st = absp_decode_step(ctx, layer, l->stage_q.p, l->stage_out.p, cap);
+        if (e == cudaSuccess && st == ABSP_OK)
+            e = cudaMemcpyAsync(out_host, l->stage_out.p, nq * sizeof(float), cudaMemcpyDeviceToHost, cap);
+        const cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+        if (e == cudaSuccess) e = e2;
+    }
+    l->host_launches = int(ctx->launches - before);
+    ctx->launches = before;  // counted when the graph runs
+    if (e == cudaSuccess && st == ABSP_OK) {
+        size_t n = 0;
+        e = cudaGraphGetNodes(graph, nullptr, &n);
+        std::vector<cudaGraphNode_t> nodes(n);
+        if (e == cudaSuccess) e = cudaGraphGetNodes(graph, nodes.data(), &n);
+        for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+            cudaGraphNodeType t;
+            e = cudaGraphNodeGetType(nodes[i], &t);
+            if (e != cudaSuccess || t != cudaGraphNodeTypeMemcpy) continue;
+            cudaMemcpy3DParms p{};
+            e = cudaGraphMemcpyNodeGetParams(nodes[i], &p);
+            if (p.kind == cudaMemcpyHostToDevice) l->h2d_node = nodes[i];
+            else if (p.kind == cudaMemcpyDeviceToHost) l->d2h_node = nodes[i];
+        }
+        if (e == cudaSuccess && (!l->h2d_node || !l->d2h_node)) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&l->host_exec, graph, 0);
+    }
+    cudaStreamDestroy(cap);
+    if (st == ABSP_OK && e == cudaSuccess) {
+        l->host_graph = graph;
+    } else if (graph) {
+        cudaGraphDestroy(graph);
+    }
+    if (st != ABSP_OK) return st;
+    if (e != cudaSuccess) {
+        l->host_exec = nullptr;
+        cudaGetLastError();  // clear; the caller runs the step eagerly
+        return ABSP_ECUDA;
+    }
+    l->host_q = q_host;
+    l->host_out = out_host;
+    return ABSP_OK;
+}
+
 absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_host,
                                   float* out_host, void* stream) {
     Layer* l;
@@ -651,10 +724,43 @@ absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_h
     ABSP_CUDA(l->stage_q.ensure(nq));
     ABSP_CUDA(l->stage_out.ensure(nq));
     const cudaStream_t s = cudaStream_t(stream);
-    ABSP_CUDA(cudaMemcpyAsync(l->stage_q.p, q_host, nq * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
-    st = absp_decode_step(ctx, layer, l->stage_q.p, l->stage_out.p, stream);
-    if (st != ABSP_OK) return st;
-    ABSP_CUDA(cudaMemcpyAsync(out_host, l->stage_out.p, nq * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (!l->host_exec && capture_host_step(ctx, layer, l, q_host, out_host, nq) != ABSP_OK)
+        l->drop_host_graph();
+    bool graph_ok = l->host_exec != nullptr;
+    if (graph_ok && (q_host != l->host_q || out_host != l->host_out)) {
+        // re-point the copy nodes; buffers the graph cannot take (e.g. pageable memory
+        // after pinned) run this call eagerly and keep the graph as it is
+        cudaError_t e = cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, q_host,
+                                                           nq * sizeof(uint16_t), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, out_host, l->stage_out.p,
+                                                   nq * sizeof(float), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) {
+            l->host_q = q_host;
+            l->host_out = out_host;
+        } else {
+            cudaGetLastError();
+            // the nodes may be half re-pointed: restore them for the next call
+            if (cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, l->host_q,
+                                                   nq * sizeof(uint16_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, l->host_out, l->stage_out.p,
+                                                   nq * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+                cudaGetLastError();
+                l->drop_host_graph();
+            }
+            graph_ok = false;
+        }
+    }
+    if (graph_ok) {
+        ABSP_CUDA(cudaGraphLaunch(l->host_exec, s));
+        ctx->launches += uint64_t(l->host_launches);
+        l->selected = true;
+    } else {  // graph capture unavailable (e.g. pageable host memory): eager launches
+        ABSP_CUDA(cudaMemcpyAsync(l->stage_q.p, q_host, nq * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+        st = absp_decode_step(ctx, layer, l->stage_q.p, l->stage_out.p, stream);
+        if (st != ABSP_OK) return st;
+        ABSP_CUDA(cudaMemcpyAsync(out_host, l->stage_out.p, nq * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
     ABSP_CUDA(cudaStreamSynchronize(s));
     return ABSP_OK;
 }

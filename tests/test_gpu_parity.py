@@ -241,8 +241,17 @@ def test_decode_step_host_matches_device(cuda):
     dev = gl.decode()
     q_host = torch.from_numpy(layer.q.view(np.int16)).pin_memory()
     out_host = torch.empty(dev.shape, dtype=torch.float32).pin_memory()
-    gl.da.decode_step_host(0, q_host, out_host)
+    gl.da.decode_step_host(0, q_host, out_host)  # captured into a graph on first use
     assert np.array_equal(out_host.numpy(), dev)
+    # other host buffers: the graph's copy nodes are re-pointed
+    q2 = q_host.clone().pin_memory()
+    out2 = torch.zeros(dev.shape, dtype=torch.float32).pin_memory()
+    gl.da.decode_step_host(0, q2, out2)
+    assert np.array_equal(out2.numpy(), dev)
+    # pageable host memory
+    out3 = torch.zeros(dev.shape, dtype=torch.float32)
+    gl.da.decode_step_host(0, torch.from_numpy(layer.q.view(np.int16).copy()), out3)
+    assert np.array_equal(out3.numpy(), dev)
 
 
 def test_synthetic_generator_matches_host_twin(cuda):
