@@ -34,6 +34,10 @@ WORKLOADS = {
     # name: batch per GPU, seq len, kv heads, G, head dim, page, candidates, budget, layers rotated
     "cfg1": dict(batch=1, n=8192, H=8, G=4, d=128, P=8, cands=(8, 16, 32), T=1024, layers=64,
                  desc="Llama-3.1-8B single layer, batch 1, 8K ctx, blocks {8,16,32}, T=1024"),
+    # a step is the decode attention of all 32 layers (one graph, layer after layer)
+    "cfg2": dict(batch=8, n=32768, H=8, G=4, d=128, P=16, cands=(16, 32, 64), T=2048, layers=32,
+                 layers_per_step=32,
+                 desc="Llama-3.1-8B all 32 layers, batch 8, 32K ctx, blocks {16,32,64}, T=2048 (assumed), int4 mean"),
     "cfg3": dict(batch=16, n=131072, H=8, G=4, d=128, P=16, cands=(16, 32, 64), T=2048, layers=4,
                  desc="Llama-3.1-8B decode attention, batch 16/GPU, 128K ctx, blocks {16,32,64}, T=2048"),
     "cfg4u": dict(batch=32, n=131072, H=8, G=4, d=128, P=16, cands=(16,), T=2048, layers=2,
@@ -173,10 +177,10 @@ def run_reference(args, w, rank, world):
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return
-    t = res["seconds_per_sequence"]
+    t = res["seconds_per_sequence"] * w.get("layers_per_step", 1)  # a token passes every layer of a step
     value = 1.0 / t  # a batch of b sequences takes b*t, producing b tokens
-    sample = (f"1 sequence of the {w['batch']}-sequence batch per step (128K ctx, layer 0); "
-              f"tokens/s = batch / (batch x per-sequence time)")
+    sample = (f"1 sequence of the {w['batch']}-sequence batch per step ({w['n']} ctx, layer 0); "
+              f"tokens/s = batch / (batch x per-sequence time x {w.get('layers_per_step', 1)} layers)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 * w["batch"],
@@ -235,22 +239,27 @@ def run_absp(args, w, rank, world, local):
     trace("layers built")
     info = da.layer_info(0)
     step_bytes, select_bytes, attn_kv_bytes = algorithmic_bytes(w, info.kv_bytes_selected, info.total_centroids, B)
+    step_bytes *= w.get("layers_per_step", 1)  # every layer of a step reads its own store and KV
     attn_bytes = attn_kv_bytes + B * H * G * d * (2 + 4)
 
-    # one CUDA graph per layer: select (score + top-k) + attend (+ merge)
+    # one CUDA graph per step (select + attend of layers_per_step layers) and, per
+    # layer, attention-only and selection-only graphs for the kernel breakdown
+    lps = w.get("layers_per_step", 1)
     graphs, sel_graphs, att_graphs = [], [], []
     launches_before = da.launch_count()
     with torch.cuda.stream(stream):
         for l in range(L):  # eager warm-up (also initialises the selection buffers)
             da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
     stream.synchronize()
-    per_step_launches = (da.launch_count() - launches_before) // L
+    per_step_launches = (da.launch_count() - launches_before) // L * lps
     trace("eager warm-up done")
-    for l in range(L):
+    for first in range(0, L, lps):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
-            da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
+            for l in range(first, first + lps):
+                da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
         graphs.append(g)
+    for l in range(L):
         _, stride, _ = da.last_selection(l)
         ga = torch.cuda.CUDAGraph()
         with torch.cuda.graph(ga, stream=stream):
@@ -293,7 +302,7 @@ def run_absp(args, w, rank, world, local):
     trace("graphs captured")
     sampler = ClockSampler(local)
     with sampler:
-        ms_step = timed(lambda i: graphs[i % L].replay(), K, W)
+        ms_step = timed(lambda i: graphs[i % len(graphs)].replay(), K, W)
     trace(f"step timed: {ms_step * 1e3:.1f} us")
     ms_attn = timed(lambda i: att_graphs[i % L].replay(), K, W)
     trace(f"attend timed: {ms_attn * 1e3:.1f} us")
@@ -305,13 +314,18 @@ def run_absp(args, w, rank, world, local):
     for l in range(L):
         q_host[l].copy_(layers[l]["q"].cpu())
     out_host = torch.empty(B, H * G, d, dtype=torch.float32).pin_memory()
-    for i in range(W):
-        da.decode_step_host(i % L, q_host[i % L], out_host, stream)
+    def host_step(i):
+        first = (i * lps) % L
+        for l in range(first, first + lps):
+            da.decode_step_host(l, q_host[l], out_host, stream)
+
+    for i in range(max(W, L // lps)):  # every layer's host graph is captured before timing
+        host_step(i)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for i in range(K):
-        da.decode_step_host(i % L, q_host[i % L], out_host, stream)
+        host_step(i)
     e2e_s = (time.perf_counter() - t0) / K
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
@@ -323,10 +337,10 @@ def run_absp(args, w, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res, err = cpu_reference(w, args.cpu_reps, 1)
         if res:
-            cpu = {"value": 1.0 / res["seconds_per_sequence"], "unit": "tokens/s", "cores": res["cores"],
+            cpu = {"value": 1.0 / (res["seconds_per_sequence"] * lps), "unit": "tokens/s", "cores": res["cores"],
                    "kind": "reference",
-                   "sample": f"1 of {B} sequences (128K ctx, layer 0), median of {args.cpu_reps} after 1 warm-up; "
-                             f"OMP over all host cores; tokens/s = 1 / per-sequence time"}
+                   "sample": f"1 of {B} sequences ({n} ctx, layer 0), median of {args.cpu_reps} after 1 warm-up; "
+                             f"OMP over all host cores; tokens/s = 1 / (per-sequence per-layer time x {lps} layers)"}
         else:
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference", "sample": err}
 
@@ -345,7 +359,7 @@ def run_absp(args, w, rank, world, local):
             "config": {"workload": args.workload, "desc": w["desc"], "batch_per_gpu": B, "global_batch": tokens,
                        "seq_len": n, "kv_heads": H, "q_heads": H * G, "head_dim": d, "page_size": P,
                        "block_sizes": assignment.block_sizes, "token_budget": T, "quant": "int4xasym",
-                       "centroids": "mean", "layers_rotated": L,
+                       "centroids": "mean", "layers_rotated": L, "layers_per_step": lps,
                        "l2": f"{L} rotating layers x {step_bytes / 1e6:.0f} MB algorithmic bytes per step (> 126 MB L2)",
                        "parallelism": f"batch-sharded x{world}, no collective",
                        "compute": "int4 codes -> exact fp32 scores; bf16 MMA (mma.sync) fp32 accumulate"},
@@ -358,7 +372,7 @@ def run_absp(args, w, rank, world, local):
                            "select_bytes": select_bytes},
             "cpu_baseline": cpu,
             "e2e": {"value": tokens / e2e_s, "unit": "tokens/s",
-                    "h2d_bytes_per_step": B * H * G * d * 2, "d2h_bytes_per_step": B * H * G * d * 4,
+                    "h2d_bytes_per_step": B * H * G * d * 2 * lps, "d2h_bytes_per_step": B * H * G * d * 4 * lps,
                     "ms_per_step": e2e_s * 1e3},
             "gpu_launches": per_step_launches * K,
             "clocks": sampler.summary(),
