@@ -108,16 +108,20 @@ cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreWork&
 cudaError_t init_score_attributes();  // per device, once
 // Selected blocks resolved to pool pages, laid out by global attention chunk:
 // unit u's slot s = entry * (B/P) + page lives at index chunk_base[u] * ns + s, so
-// chunk w's slots are [w * ns, (w + 1) * ns).
+// chunk w's slots are [w * ns, (w + 1) * ns). Written by the top-k kernel (decode
+// step) or k_resolve_pages (explicit selections), read by the attention producer.
 struct PageList {
     uint32_t* page;               // head * pool_pages + pool page id
     uint16_t* valid;              // valid rows of the page (0 = empty slot)
     const uint32_t* chunk_base;   // [units + 1] first chunk of each unit (work list)
     uint32_t ns;                  // page slots per chunk = kAttnChunkRows / P
 };
+// ready (decode step, else null): per-unit "selection published" flags, raised by the
+// selection kernel after the unit's blocks and page list are written (release) and
+// re-armed by the attention merge; the attention producer starts a unit on its flag.
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                        cudaStream_t s, int* launches);
+                        uint32_t* ready, cudaStream_t s, int* launches);
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
                                  const uint32_t* counts, const PageList& pages, cudaStream_t s,
                                  int* launches);
@@ -133,9 +137,8 @@ struct AttendWork {
     uint32_t grid;               // persistent CTAs: min(n_work, SMs); CTA c owns chunks
                                  // [c * n_work / grid, (c + 1) * n_work / grid)
 };
-cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages,
-                          const uint32_t* counts, const AttendWork& work,
-                          float* part_o, float* part_ml, float* out, cudaStream_t s,
+cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages, uint32_t* ready,
+                          const AttendWork& work, float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches);
 size_t attend_smem_bytes(uint32_t D, uint32_t P);
 // Decode-step selection via tensor-core filter + exact refine (select.cu): same
@@ -144,7 +147,7 @@ bool select_fast_supported(const LayerView& L, uint32_t max_nblocks, uint32_t ma
 cudaError_t init_select_attributes();  // per device, once
 cudaError_t launch_select_fast(const LayerView& L, const uint16_t* q, const ScoreWork& work, float* approx,
                                float* err, uint32_t* blocks, uint32_t stride, uint32_t* counts,
-                               const PageList& pages, cudaStream_t s, int* launches);
+                               const PageList& pages, uint32_t* ready, cudaStream_t s, int* launches);
 cudaError_t init_attend_attributes();  // per device, once
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);

@@ -116,6 +116,7 @@ struct Layer {
     DevBuf<float> values, values_min, scales, zps, scales_min, zps_min, scores;
     DevBuf<uint32_t> codes, codes_min;
     DevBuf<uint32_t> sel_blocks, sel_counts;
+    DevBuf<uint32_t> ready;  // decode step: per-unit "selection published" flags (zero between steps)
     DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
     DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
@@ -142,7 +143,7 @@ struct Layer {
         values.release(); values_min.release(); scales.release(); zps.release();
         scales_min.release(); zps_min.release(); scores.release();
         codes.release(); codes_min.release();
-        sel_blocks.release(); sel_counts.release();
+        sel_blocks.release(); sel_counts.release(); ready.release();
         approx.release(); unit_err.release();
         part_o.release(); part_ml.release();
         stage_q.release(); stage_out.release();
@@ -247,19 +248,19 @@ absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t c
         wl.max_runs = std::max(wl.max_runs, last - first + 1);
     }
     const size_t n_slots = size_t(wl.n_work) * wl.ns;
+    ABSP_CUDA(wl.page.ensure(n_slots));
+    ABSP_CUDA(wl.valid.ensure(n_slots));
+    ABSP_CUDA(cudaMemset(wl.valid.p, 0, n_slots * 2));
     ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
     ABSP_CUDA(wl.chunk_idx.ensure(idx_of.size()));
     ABSP_CUDA(wl.chunk_base.ensure(base.size()));
     ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
     ABSP_CUDA(wl.unit_run.ensure(l.desc.size()));
-    ABSP_CUDA(wl.page.ensure(n_slots));
-    ABSP_CUDA(wl.valid.ensure(n_slots));
     ABSP_CUDA(cudaMemcpy(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemcpy(wl.unit_run.p, run.data(), run.size() * 4, cudaMemcpyHostToDevice));
     ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
-    ABSP_CUDA(cudaMemset(wl.valid.p, 0, n_slots * 2));
     // one partial slot per (unit, CTA run, consumer warp)
     ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 8 * D));
     ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 16));
@@ -521,6 +522,8 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
     ABSP_CUDA(l->sel_counts.ensure(units));
+    ABSP_CUDA(l->ready.ensure(units));
+    ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
     for (auto& kv : l->attend_work) kv.second.release();
     l->attend_work.clear();
     st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
@@ -550,25 +553,28 @@ absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream) {
 }
 
 // Scoring + top-k; the top-k kernel also resolves the selection into the decode
-// work list's page list, consumed by the attention producer.
-static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* blocks,
-                             uint32_t stride, uint32_t* counts, cudaStream_t s) {
+// work list's page list, consumed by the attention producer. In the decode step
+// (ready != null) it then raises the unit's ready flag, and the attention kernel
+// starts on the unit right then.
+static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* blocks, uint32_t stride,
+                             uint32_t* counts, uint32_t* ready, cudaStream_t s) {
     const LayerView v = view_of(ctx, *l);
     int n = 0;
     const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1)};
     cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), sw, s, &n);
     if (e == cudaSuccess)
-        e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), s, &n);
+        e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), ready, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "select kernels");
     return ABSP_OK;
 }
 
-static absp_status do_attend_step(absp_ctx* ctx, Layer* l, const void* q, float* out, cudaStream_t s) {
+// Attention over the layer's own selection buffers.
+static absp_status do_attend_step(absp_ctx* ctx, Layer* l, const void* q, float* out, uint32_t* ready,
+                                  cudaStream_t s) {
     int n = 0;
-    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->step_work.pages(),
-                                  l->sel_counts.p, work_view(l->step_work), l->part_o.p,
-                                  l->part_ml.p, out, s, &n);
+    cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->step_work.pages(), ready,
+                                  work_view(l->step_work), l->part_o.p, l->part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
@@ -585,7 +591,7 @@ absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* 
         return fail(ABSP_EINVAL, "select: blocks_stride " + std::to_string(blocks_stride) +
                                      " < max_select " + std::to_string(l->max_select));
     DeviceGuard dg(ctx->device);
-    st = do_select(ctx, l, q, blocks, blocks_stride, counts, cudaStream_t(stream));
+    st = do_select(ctx, l, q, blocks, blocks_stride, counts, nullptr, cudaStream_t(stream));
     if (st == ABSP_OK) l->selected = true;
     return st;
 }
@@ -599,8 +605,8 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     if (!q || !blocks || !counts || !out) return fail(ABSP_EINVAL, "attend: null pointer");
     if (blocks_stride == 0) return fail(ABSP_EINVAL, "attend: blocks_stride must be positive");
     DeviceGuard dg(ctx->device);
-    // Work list + page list for selections of up to min(N, blocks_stride) entries
-    // per unit; built once per stride (the first call for a new stride allocates).
+    // Work list for selections of up to min(N, blocks_stride) entries per unit; built
+    // once per stride (the first call for a new stride allocates).
     auto it = l->attend_work.find(blocks_stride);
     if (it == l->attend_work.end()) {
         st = build_work(*l, ctx->cfg.head_dim, ctx->cfg.page_size, false, blocks_stride, ctx->num_sms,
@@ -613,8 +619,8 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     int n = 0;
     cudaError_t e = launch_resolve_pages(v, blocks, blocks_stride, counts, it->second.pages(), s, &n);
     if (e == cudaSuccess)
-        e = launch_attend(v, static_cast<const uint16_t*>(q), it->second.pages(), counts,
-                          work_view(it->second), l->part_o.p, l->part_ml.p, out, s, &n);
+        e = launch_attend(v, static_cast<const uint16_t*>(q), it->second.pages(), nullptr, work_view(it->second),
+                          l->part_o.p, l->part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
@@ -628,7 +634,7 @@ absp_status absp_attend_selected(absp_ctx* ctx, uint32_t layer, const void* q, f
     if (!l->selected) return fail(ABSP_ESTATE, "attend_selected: no selection made on this layer");
     if (!q || !out) return fail(ABSP_EINVAL, "attend_selected: null pointer");
     DeviceGuard dg(ctx->device);
-    return do_attend_step(ctx, l, q, out, cudaStream_t(stream));
+    return do_attend_step(ctx, l, q, out, nullptr, cudaStream_t(stream));
 }
 
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
@@ -645,16 +651,16 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
         const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1)};
         int n = 0;
         cudaError_t e = launch_select_fast(v, static_cast<const uint16_t*>(q), sw, l->approx.p, l->unit_err.p,
-                                           l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->step_work.pages(), s,
-                                           &n);
+                                           l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->step_work.pages(),
+                                           l->ready.p, s, &n);
         ctx->launches += n;
         if (e != cudaSuccess) return cuda_fail(e, "select kernels");
     } else {
-        st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, s);
+        st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->ready.p, s);
         if (st != ABSP_OK) return st;
     }
     l->selected = true;
-    return do_attend_step(ctx, l, q, out, s);
+    return do_attend_step(ctx, l, q, out, l->ready.p, s);
 }
 
 // Captures H2D q -> absp_decode_step -> D2H out of `layer` into a graph (host

@@ -17,7 +17,9 @@
 //              prefetched with independent loads) and issues one cp.async.bulk per
 //              page for K and V — the TMA bulk-copy engine, 1 instruction per 1-4 KB
 //              page — plus one for the unit's G query rows, completing on the
-//              stage's full barrier. (A copy-only probe of this pipeline streams
+//              stage's full barrier. In the decode step a unit is started as soon
+//              as its selection is published (per-unit ready flag, acquire), not
+//              when the whole top-k grid has finished. (A copy-only probe of this pipeline streams
 //              scattered 4 KB pages at 97% of measured HBM bandwidth.)
 //   consumers: warp w owns rows [16w, 16w+16) of every chunk and is an independent
 //              split with its own fp32 online-softmax state: S^T = K Q^T on
@@ -72,6 +74,12 @@ __device__ __forceinline__ unsigned long long gtime() {
 #else
 #define ATTN_TRACE(slot) do {} while (0)
 #endif
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
     uint32_t old;
@@ -138,7 +146,7 @@ __device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
-                                                      PageList pages,
+                                                      PageList pages, uint32_t* __restrict__ ready,
                                                       const uint32_t* __restrict__ chunk_unit,
                                                       const uint32_t* __restrict__ chunk_idx,
                                                       const uint32_t* __restrict__ chunk_base,
@@ -172,7 +180,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     if (tid == 0) ATTN_TRACE(0);
     griddep_launch_dependents();
     __syncthreads();
-    griddep_wait();  // page lists, q, partial buffers and unit counters are step data
+    // Page lists, q, partial buffers and unit counters are step data. In the decode step
+    // the per-unit ready flags order this kernel after its predecessors (a flag is
+    // raised after the top-k kernel's own wait); otherwise wait for the previous grid.
+    if (!ready) griddep_wait();
 
     if (warp == kWarps) {
         // ============================ producer ================================
@@ -184,10 +195,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         struct Pref {
             uint32_t u, c, gp[SPL], vl[SPL];
         };
+        uint32_t pu = 0xffffffffu;  // last unit whose ready flag was acquired
         auto fetch = [&](uint32_t w, Pref& f) {
             if (w >= w_end) return;
             f.u = __ldg(chunk_unit + w);
             f.c = __ldg(chunk_idx + w);
+            if (ready && f.u != pu) {  // decode step: the unit's page list must be published
+                pu = f.u;
+                while (ld_acquire(ready + pu) == 0u) __nanosleep(32);
+            }
             const size_t base = size_t(w) * NS;
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
@@ -208,8 +224,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 gp[k] = f0.gp[k];
                 vl[k] = f0.vl[k];
             }
-            f0 = f1;
-            fetch(w + 2, f1);
             mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
             StageMeta& mt = sh.meta[stage];
             const uint32_t kdst = smem_base + stage * 2 * TB;
@@ -245,6 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 stage = 0;
                 phase ^= 1;
             }
+            // chunk w+2's page list: after the issue, so a flag wait never delays chunk w
+            f0 = f1;
+            fetch(w + 2, f1);
         }
         return;
     }
@@ -351,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                                                           acc[3 % PER] * inv);
         else
             *reinterpret_cast<float2*>(dst) = make_float2(acc[0] * inv, acc[1 % PER] * inv);
+        if (ready && h == 0 && lane == 0) ready[mu] = 0u;  // every producer is past mu: re-arm
     };
 
     // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count its
@@ -535,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     const uint32_t npend = min(sh.npend, uint32_t(kMaxPend));
     for (uint32_t j = warp; j < npend * G; j += kWarps) merge(sh.pend[j / G], j % G);
     if (lane == 0) ATTN_TRACE(242 + warp);  // per-warp end (merges done)
+    if (ready) griddep_wait();  // complete only after the selection grid (clean ordering downstream)
 }
 
 }  // namespace
@@ -558,18 +577,17 @@ cudaError_t init_attend_attributes() {
                                 int(attend_smem_bytes(128, 1)));
 }
 
-cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages,
-                          const uint32_t* counts, const AttendWork& wk, float* part_o,
-                          float* part_ml, float* out, cudaStream_t s, int* launches) {
-    (void)counts;  // chunk page lists carry the selection (empty slots have valid = 0)
+cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages, uint32_t* ready,
+                          const AttendWork& wk, float* part_o, float* part_ml, float* out, cudaStream_t s,
+                          int* launches) {
     const size_t smem = attend_smem_bytes(L.D, L.P);
     const uint32_t grid = wk.grid;  // = min(n_work, SMs): the CTA runs in unit_run assume it
     if (grid == 0) return cudaSuccess;
     if (L.D == 64)
-        launch_pdl(k_attn<64>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, wk.chunk_unit, wk.chunk_idx,
+        launch_pdl(k_attn<64>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, ready, wk.chunk_unit, wk.chunk_idx,
                    wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, part_o, part_ml, wk.unit_done, out);
     else
-        launch_pdl(k_attn<128>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, wk.chunk_unit, wk.chunk_idx,
+        launch_pdl(k_attn<128>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, ready, wk.chunk_unit, wk.chunk_idx,
                    wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, part_o, part_ml, wk.unit_done, out);
     ++*launches;
     return cudaGetLastError();

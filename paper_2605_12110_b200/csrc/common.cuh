@@ -73,4 +73,22 @@ __device__ __forceinline__ void resolve_pages(const LayerView& L, const UnitDesc
     }
 }
 
+// Publishes unit u's ordered selection `outs` (shared memory): blocks / counts, the
+// page list for the attention producer and, in the decode step, the unit's ready
+// flag (CTA barrier, then one gpu-scope fence + release store by thread 0).
+__device__ __forceinline__ void publish_selection(const LayerView& L, const UnitDesc& du, uint32_t u,
+                                                  const uint32_t* outs, uint32_t n, uint32_t* blocks, uint32_t stride,
+                                                  uint32_t* counts, const PageList& pages, uint32_t* ready) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) blocks[size_t(u) * stride + i] = outs[i];
+    if (threadIdx.x == 0) counts[u] = n;
+    resolve_pages(L, du, u, n, outs, pages);
+    if (!ready) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(ready + u), "r"(1u) : "memory");
+    }
+}
+
 }  // namespace absp

@@ -22,7 +22,7 @@
 //                    {A_i >= a - 2E} (typically K-1 plus a few) are re-scored with
 //                    the reference's exact serial arithmetic (product table), and
 //                    the exact top-(K-1) by (score desc, index asc) plus the
-//                    trailing block N-1 is taken among them, ordered, written and
+//                    trailing block N-1 is taken among them, ordered, published and
 //                    resolved to pages. Degenerate inputs with more candidates than
 //                    fit (mass near-ties) re-score every block instead.
 //
@@ -473,7 +473,8 @@ template <int D, bool ASYM>
 __global__ void __launch_bounds__(kRThreads, 1) k_select_refine(LayerView L, const uint16_t* __restrict__ q,
                                                                 const float* __restrict__ approx,
                                                                 const float* __restrict__ err, uint32_t* blocks,
-                                                                uint32_t stride, uint32_t* counts, PageList pages) {
+                                                                uint32_t stride, uint32_t* counts, PageList pages,
+                                                                uint32_t* ready) {
     using C = RefineCfg<D>;
     constexpr int W = D / 8, U = W / 4, LV = 16;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -653,9 +654,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_select_refine(LayerView L, con
     const uint32_t sel_total = all ? N : K;
     __syncthreads();
     REFINE_TRACE(6);
-    for (uint32_t j = tid; j < sel_total; j += kRThreads) blocks[size_t(u) * stride + j] = outs[j];
-    if (tid == 0) counts[u] = sel_total;
-    resolve_pages(L, du, u, sel_total, outs, pages);
+    publish_selection(L, du, u, outs, sel_total, blocks, stride, counts, pages, ready);
     REFINE_TRACE(7);
 #ifdef ABSP_ATTN_TRACE
     if (tid == 0 && blockIdx.x < 1024) g_refine_cand[blockIdx.x] = Cn;
@@ -673,12 +672,14 @@ cudaError_t attrs_d() {
 
 template <int D, bool ASYM>
 cudaError_t launch_d(const LayerView& L, const uint16_t* q, const ScoreWork& w, float* approx, float* err,
-                     uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages, cudaStream_t s) {
+                     uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages, uint32_t* ready,
+                     cudaStream_t s) {
     cudaError_t e = launch_pdl(k_score_approx<D, ASYM>, dim3(w.grid), dim3(kABlock), ApproxCfg<D>::SMEM, s, L, q, w,
                                approx, err);
     if (e != cudaSuccess) return e;
     return launch_pdl(k_select_refine<D, ASYM>, dim3(L.units), dim3(kRThreads), RefineCfg<D>::SMEM, s, L, q,
-                      static_cast<const float*>(approx), static_cast<const float*>(err), blocks, stride, counts, pages);
+                      static_cast<const float*>(approx), static_cast<const float*>(err), blocks, stride, counts, pages,
+                      ready);
 }
 
 }  // namespace
@@ -706,16 +707,16 @@ cudaError_t init_select_attributes() {
 
 cudaError_t launch_select_fast(const LayerView& L, const uint16_t* q, const ScoreWork& work, float* approx, float* err,
                                uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                               cudaStream_t s, int* launches) {
+                               uint32_t* ready, cudaStream_t s, int* launches) {
     *launches += 2;
     const bool asym = L.mode == ABSP_QUANT_ASYM;
     cudaError_t e;
     if (L.D == 64)
-        e = asym ? launch_d<64, true>(L, q, work, approx, err, blocks, stride, counts, pages, s)
-                 : launch_d<64, false>(L, q, work, approx, err, blocks, stride, counts, pages, s);
+        e = asym ? launch_d<64, true>(L, q, work, approx, err, blocks, stride, counts, pages, ready, s)
+                 : launch_d<64, false>(L, q, work, approx, err, blocks, stride, counts, pages, ready, s);
     else
-        e = asym ? launch_d<128, true>(L, q, work, approx, err, blocks, stride, counts, pages, s)
-                 : launch_d<128, false>(L, q, work, approx, err, blocks, stride, counts, pages, s);
+        e = asym ? launch_d<128, true>(L, q, work, approx, err, blocks, stride, counts, pages, ready, s)
+                 : launch_d<128, false>(L, q, work, approx, err, blocks, stride, counts, pages, ready, s);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -21,9 +21,10 @@
 //   3. The <= K winners become 64-bit composite keys (key << 32 | ~index), all
 //      distinct; their rank among each other is their output position (rank sort
 //      for K <= 256, bitonic sort above), which is exactly the reference order.
-//   4. The kernel also resolves every selected block to its pool pages (the
-//      reference's populate_page_spans, engine.cpp:271-283) for the attention
-//      producer: page id and valid-row count per page slot.
+//   4. The selection is published from shared memory with every selected block
+//      resolved to its pool pages (the reference's populate_page_spans,
+//      engine.cpp:271-283) for the attention producer; in the decode step the
+//      unit's ready flag then lets the attention producer start on it.
 #include "absp_internal.cuh"
 #include "ptx.cuh"
 #include "common.cuh"
@@ -58,6 +59,7 @@ struct TopkSmem {
     uint32_t state[6];  // prefix, pmask, remaining, eq_total, compacted count, compact flag
     uint32_t nsel;
     unsigned long long sel[kMaxSort];
+    uint32_t outs[kMaxSort];  // the ordered selection, published from here
     union {
         uint32_t eq[kMaxSteps];
         struct {
@@ -92,7 +94,7 @@ __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t pr
 
 template <bool REG, int ITEMS>
 __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
-                                                   uint32_t* counts, PageList pages) {
+                                                   uint32_t* counts, PageList pages, uint32_t* ready) {
     __shared__ TopkSmem sm;
     TOPK_TRACE(0);
     const uint32_t u = blockIdx.x;
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
 
     griddep_launch_dependents();
     griddep_wait();  // the scores are written by the scoring kernel of this step
+    const float tail_score = N > K ? __ldg(sc + N - 1) : 0.0f;  // the trailing block, loaded early
     Keys<REG, ITEMS> keys;
     keys.sc = sc;
     keys.n_cand = n_cand;
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
             }
             __syncthreads();
             TOPK_TRACE(3);
-            const unsigned long long ct = (uint64_t(order_key(sc[N - 1])) << 32) | uint32_t(~(N - 1));
-            uint32_t* out = blocks + size_t(u) * stride;
+            const unsigned long long ct = (uint64_t(order_key(tail_score)) << 32) | uint32_t(~(N - 1));
+            uint32_t* out = sm.outs;
             if (C <= 256) {
                 // rank among candidates = output position (composites are distinct)
                 for (uint32_t p = threadIdx.x; p < C; p += kThreads) {
@@ -279,9 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
             if (threadIdx.x == 0) {
                 out[sm.nsel] = N - 1;  // the trailing block sits after every larger winner
                 TOPK_TRACE(4);
-                counts[u] = K;
             }
-            resolve_pages(L, du, u, K, out, pages);
+            publish_selection(L, du, u, out, K, blocks, stride, counts, pages, ready);
             TOPK_TRACE(5);
             return;
         }
@@ -494,13 +496,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
         }
         if (threadIdx.x == 0) {
             const uint32_t t = N - 1;
-            sm.sel[K - 1] = (uint64_t(order_key(sc[t])) << 32) | uint32_t(~t);
+            sm.sel[K - 1] = (uint64_t(order_key(tail_score)) << 32) | uint32_t(~t);
         }
     }
     __syncthreads();
 
     // ---- order: (key desc, index asc) == composite desc -----------------------
-    uint32_t* out = blocks + size_t(u) * stride;
+    uint32_t* out = sm.outs;
     if (sel_total <= 256) {
         // rank sort: position = number of larger composites (all distinct)
         for (uint32_t i = threadIdx.x; i < sel_total; i += kThreads) {
@@ -532,8 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
         }
         for (uint32_t i = threadIdx.x; i < sel_total; i += kThreads) out[i] = ~uint32_t(sm.sel[i]);
     }
-    if (threadIdx.x == 0) counts[u] = sel_total;
-    resolve_pages(L, du, u, sel_total, out, pages);
+    publish_selection(L, du, u, out, sel_total, blocks, stride, counts, pages, ready);
 }
 
 }  // namespace
@@ -546,12 +547,13 @@ cudaError_t debug_topk_trace(void* dst, size_t bytes) {
 
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
+                        uint32_t* ready,
                         cudaStream_t s, int* launches) {
     if (max_budget > uint32_t(kMaxSort) || max_nblocks > uint32_t(kMaxSteps) * 32u)
         return cudaErrorInvalidValue;
     const uint32_t per_thread = (max_nblocks + kThreads - 1) / kThreads;
     const dim3 grid(L.units);
-#define ABSP_TOPK(REG, IT) launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages)
+#define ABSP_TOPK(REG, IT) launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages, ready)
     if (per_thread <= 1) ABSP_TOPK(true, 1);
     else if (per_thread <= 2) ABSP_TOPK(true, 2);
     else if (per_thread <= 4) ABSP_TOPK(true, 4);
@@ -594,7 +596,6 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
         pages.valid[base + s] = uint16_t(v);
     }
 }
-
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
                                  const uint32_t* counts, const PageList& pages, cudaStream_t s,
                                  int* launches) {

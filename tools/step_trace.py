@@ -1,0 +1,73 @@
+"""Whole decode-step timeline (debug): one cfg-3 decode step with lib/libabsp_trace.so after
+an L2 flush; scorer, top-k and attention per-CTA globaltimer stamps on one time base.
+Tooling, not product."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2605_12110_b200 import _abi  # noqa: E402
+
+_abi._lib = _abi.load(ROOT / "paper_2605_12110_b200" / "lib" / "libabsp_trace.so")
+for f in ("absp_debug_score_trace", "absp_debug_topk_trace", "absp_debug_attn_trace"):
+    getattr(_abi._lib, f).argtypes = [C.c_void_p, C.c_size_t]
+from bench import SEED, WORKLOADS  # noqa: E402
+from paper_2605_12110_b200 import (BlockAssignment, DecodeAttention, EngineConfig, QuantSpec,  # noqa: E402
+                                   fill_synthetic_bf16)
+
+w = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg3"]
+B, n, H, G, d, P, T = w["batch"], w["n"], w["H"], w["G"], w["d"], w["P"], w["T"]
+pages = B * ((n + P - 1) // P)
+cfg = EngineConfig(num_heads=H, head_dim=d, page_size=P, candidate_block_sizes=tuple(w["cands"]), token_budget=T,
+                   quant=QuantSpec(4), num_q_heads=H * G, max_batch=B, max_seq_len=n)
+da = DecodeAttention(cfg)
+da.set_assignment(0, BlockAssignment.cycled(H, w["cands"]))
+k = torch.empty(H, pages, P, d, dtype=torch.int16, device="cuda")
+v = torch.empty_like(k)
+q = torch.empty(B, H * G, d, dtype=torch.int16, device="cuda")
+for t, s in ((k, 0), (v, 1), (q, 2)):
+    fill_synthetic_bf16(t, SEED, s)
+pt = torch.arange(pages, dtype=torch.int32, device="cuda").reshape(B, -1)
+da.bind(0, k, v, pt, [n] * B)
+da.build_store(0)
+out = torch.empty(B, H * G, d, dtype=torch.float32, device="cuda")
+stream = torch.cuda.Stream()
+with torch.cuda.stream(stream):
+    for _ in range(3):
+        da.decode_step(0, q, out, stream)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        da.decode_step(0, q, out, stream)
+flush = torch.empty(1 << 28, dtype=torch.int8, device="cuda")
+pct = lambda a: " ".join(f"{x:7.2f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
+for rep in range(2):
+    flush.fill_(rep)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    sc = np.zeros((320, 16), np.uint64)
+    tk = np.zeros((1024, 8), np.uint64)
+    at = np.zeros((160, 256), np.uint64)
+    _abi.check(_abi._lib.absp_debug_score_trace(sc.ctypes.data, sc.nbytes))
+    _abi.check(_abi._lib.absp_debug_topk_trace(tk.ctypes.data, tk.nbytes))
+    _abi.check(_abi._lib.absp_debug_attn_trace(at.ctypes.data, at.nbytes))
+    ns = 2 * 148
+    t0 = int(sc[:ns, 0].min())
+    r = lambda a: (a.astype(np.int64) - t0) / 1e3
+    units = B * H
+    print(f"rep {rep} (us from the first scorer CTA start; pctl 0/10/50/90/100)")
+    print(f"  scorer start      {pct(r(sc[:ns, 0]))}")
+    print(f"  scorer end        {pct(r(sc[:ns, 1]))}")
+    print(f"  topk start        {pct(r(tk[:units, 0]))}")
+    print(f"  topk end (pages)  {pct(r(tk[:units, 5][tk[:units, 5] > 0]))}")
+    print(f"  attn CTA start    {pct(r(at[:148, 0]))}")
+    first = np.array([at[c, 64] for c in range(148)])
+    print(f"  attn first data   {pct(r(first))}")
+    last_arr = np.array([max(at[c, 64:128]) for c in range(148)])
+    print(f"  attn last data    {pct(r(last_arr))}")
+    ends = np.array([max(at[c, 242:250]) for c in range(148)])
+    print(f"  attn end          {pct(r(ends))}")
