@@ -62,9 +62,12 @@ for rep in range(2):
     print(f"rep {rep} (us from the first scorer CTA start; pctl 0/10/50/90/100)")
     print(f"  scorer start      {pct(r(sc[:ns, 0]))}")
     print(f"  scorer end        {pct(r(sc[:ns, 1]))}")
-    print(f"  topk start        {pct(r(tk[:units, 0]))}")
-    print(f"  topk end (pages)  {pct(r(tk[:units, 5][tk[:units, 5] > 0]))}")
+    if tk[:units, 0].max() >= sc[:ns, 0].min():
+        print(f"  topk start        {pct(r(tk[:units, 0]))}")
+        print(f"  topk end (pages)  {pct(r(tk[:units, 5][tk[:units, 5] > 0]))}")
     print(f"  attn CTA start    {pct(r(at[:148, 0]))}")
+    if at[:148, 250].max() > 0:
+        print(f"  attn selected     {pct(r(at[:148, 250][at[:148, 250] > 0]))}")
     first = np.array([at[c, 64] for c in range(148)])
     print(f"  attn first data   {pct(r(first))}")
     last_arr = np.array([max(at[c, 64:128]) for c in range(148)])
