@@ -13,6 +13,9 @@
  *                                                             kv_cache.hpp:26-67
  *   absp_build_store       <- compute_block_centroids         centroids.hpp:56-57
  *                             + quantize_store                quantizer.hpp:43
+ *   absp_append            <- PagedKVCache::append            kv_cache.cpp:44-70
+ *                             + refresh_tail_centroids        centroids.cpp:158-163
+ *                             + requantize_heads (all heads)  quantizer.cpp:113-150
  *   absp_select            <- estimate_scores(q, qstore)      engine.hpp:47-49
  *                             + select_topk                   engine.hpp:61-64
  *   absp_attend            <- populate_page_spans             engine.hpp:71
@@ -142,6 +145,17 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
 /* Prefill-time centroid build + quantization (compute_block_centroids +
  * quantize_store) for every (sequence, KV head) of the layer. */
 absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream);
+
+/* Decode-time append + store maintenance, the first half of DecodeEngine::step
+ * (engine.cpp:443-449): appends one token per sequence — k_new / v_new bf16
+ * [batch][num_kv_heads][head_dim] (device) are written to row n % P of page
+ * page_table[b][n / P] (PagedKVCache::append, kv_cache.cpp:44-70; the caller's
+ * page table must map position n) — then refresh_tail_centroids and
+ * requantize_heads over every head (centroids.cpp:122-163, quantizer.cpp:113-150),
+ * leaving the store equal to one built from scratch on the grown cache. ECAPACITY
+ * when a sequence would exceed max_seq_len or its page table. Synchronises the
+ * stream (the host-side unit layout grows with the sequences). */
+absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const void* v_new, void* stream);
 
 /* estimate_scores on the group-summed query + select_topk for every
  * (sequence, KV head). Writes blocks/counts (device). blocks_stride >= info.max_select. */

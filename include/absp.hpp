@@ -14,6 +14,7 @@
  *                                                              quantizer.hpp:43)
  *     select        = estimate_scores + select_topk             (engine.hpp:47-68)
  *     attend        = populate_page_spans + sparse_attention     (engine.hpp:71-82)
+ *     append        = DecodeEngine::step's append + refresh + requantize (engine.cpp:443-449)
  *     decode_step   = DecodeEngine::step's estimate->select->attend (engine.cpp:450-461)
  *
  * Errors are rethrown as the reference's exception classes:
@@ -272,6 +273,11 @@ class DecodeAttention {
                            seq_lens.data(), uint32_t(seq_lens.size())));
     }
     void build_store(uint32_t layer, void* stream = nullptr) { check(absp_build_store(ctx_, layer, stream)); }
+    // One token per sequence (bf16 [batch][H][d], device) + refresh_tail_centroids +
+    // requantize_heads: the maintenance half of DecodeEngine::step (engine.cpp:443-449).
+    void append(uint32_t layer, const void* k_new, const void* v_new, void* stream = nullptr) {
+        check(absp_append(ctx_, layer, k_new, v_new, stream));
+    }
     void select(uint32_t layer, const void* q, uint32_t* blocks, uint32_t stride, uint32_t* counts,
                 void* stream = nullptr) {
         check(absp_select(ctx_, layer, q, blocks, stride, counts, stream));

@@ -344,6 +344,55 @@ class RefSeq:
         return out
 
 
+class RefEngine:
+    """The reference's own DecodeEngine (engine.hpp:99-129, via ref_shim.cpp): prefill,
+    step (append + refresh_tail_centroids + requantize_heads + estimate -> select ->
+    attend, or the fp64 full attention while seq_len <= T) and a store snapshot."""
+
+    def __init__(self, H, d, P, candidates, token_budget, block_sizes, capacity, method=0, bits=4, mode=1):
+        self.H, self.d = H, d
+        self.max_k = int(token_budget // min(candidates) + 1)
+        cands = (_sz * len(candidates))(*[int(c) for c in candidates])
+        bs = (_sz * H)(*[int(b) for b in block_sizes])
+        h = C.c_void_p()
+        _rcheck(ref().ref_engine_create(H, d, P, cands, len(candidates), token_budget, method, bits, mode, bs,
+                                        capacity, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().ref_engine_destroy(self.h)
+            self.h = None
+
+    def prefill(self, keys, values, num_tokens):
+        keys = np.ascontiguousarray(keys, np.float32)
+        values = np.ascontiguousarray(values, np.float32)
+        _rcheck(ref().ref_engine_prefill(self.h, keys, values, num_tokens, keys.shape[1]))
+
+    def step(self, k, v, q):
+        out = np.zeros((self.H, self.d), np.float32)
+        blocks = np.zeros((self.H, self.max_k), np.uint32)
+        counts = np.zeros(self.H, np.uint32)
+        fb = C.c_int()
+        _rcheck(ref().ref_engine_step(self.h, np.ascontiguousarray(k, np.float32), np.ascontiguousarray(v, np.float32),
+                                      np.ascontiguousarray(q, np.float32), out, blocks.ctypes.data, self.max_k,
+                                      counts.ctypes.data, C.byref(fb)))
+        return out, [blocks[h, :counts[h]].copy() for h in range(self.H)], bool(fb.value)
+
+    def store(self):
+        total = _sz()
+        _rcheck(ref().ref_engine_store(self.h, None, None, None, None, None, C.byref(total)))
+        t = int(total.value)
+        offsets = np.zeros(self.H + 1, np.uint64)
+        values = np.zeros((t, self.d), np.float32)
+        codes = np.zeros((t, self.d), np.uint8)
+        scales = np.zeros((self.H, self.d), np.float32)
+        zps = np.zeros((self.H, self.d), np.float32)
+        _rcheck(ref().ref_engine_store(self.h, offsets.ctypes.data, values.ctypes.data, codes.ctypes.data,
+                                       scales.ctypes.data, zps.ctypes.data, None))
+        return dict(offsets=offsets, values=values, codes=codes, scales=scales, zps=zps)
+
+
 def ref_generate_synthetic(n, H, d, profiles, signal=8.0, seed=0, scatter_gap=64):
     """generate_synthetic (workload.cpp:192-249). profiles: list of ("uniform",) |
     ("clustered", count, width) | ("scattered", hot). Returns keys, values [H][n][d], queries [H][d]."""

@@ -3,11 +3,11 @@
 See DESIGN.md. The numeric path lives in lib/libabsp.so (built from csrc/ by
 build.py); this package is the Python host mirror of the reference API.
 """
-from .absparse import (BlockAssignment, CentroidMethod, DecodeAttention, EngineConfig,  # noqa: F401
-                       QuantMode, QuantSpec, build_offsets, fill_synthetic_bf16)
+from .absparse import (BlockAssignment, CentroidMethod, DecodeAttention, DecodeEngine, EngineConfig,  # noqa: F401
+                       QuantMode, QuantSpec, StepResult, build_offsets, fill_synthetic_bf16)
 from ._abi import (AbspError, CapacityError, CudaError, InvalidArgument, LogicError,  # noqa: F401
                    OutOfRange)
 
-__all__ = ["BlockAssignment", "CentroidMethod", "DecodeAttention", "EngineConfig", "QuantMode",
-           "QuantSpec", "build_offsets", "fill_synthetic_bf16", "AbspError", "CapacityError",
+__all__ = ["BlockAssignment", "CentroidMethod", "DecodeAttention", "DecodeEngine", "EngineConfig", "QuantMode",
+           "QuantSpec", "StepResult", "build_offsets", "fill_synthetic_bf16", "AbspError", "CapacityError",
            "CudaError", "InvalidArgument", "LogicError", "OutOfRange"]

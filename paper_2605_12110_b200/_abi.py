@@ -22,7 +22,7 @@ ABSP_MAX_CANDIDATES = 16
 
 EXPORTED = [
     "absp_abi_version", "absp_last_error", "absp_config_validate", "absp_ctx_create",
-    "absp_ctx_destroy", "absp_set_assignment", "absp_kv_bind", "absp_build_store", "absp_select",
+    "absp_ctx_destroy", "absp_set_assignment", "absp_kv_bind", "absp_build_store", "absp_append", "absp_select",
     "absp_attend", "absp_attend_selected", "absp_decode_step", "absp_decode_step_host", "absp_last_selection",
     "absp_get_layer_info", "absp_download_store", "absp_download_scores", "absp_download_selection", "absp_download_filter_scores",
     "absp_fill_synthetic_bf16", "absp_launch_count",
@@ -112,6 +112,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
     L.absp_set_assignment.argtypes = [vp, u32, u32p]
     L.absp_kv_bind.argtypes = [vp, u32, vp, vp, u64, vp, u32, u32p, u32]
     L.absp_build_store.argtypes = [vp, u32, vp]
+    L.absp_append.argtypes = [vp, u32, vp, vp, vp]
     L.absp_select.argtypes = [vp, u32, vp, vp, u32, vp, vp]
     L.absp_attend.argtypes = [vp, u32, vp, vp, u32, vp, vp, vp]
     L.absp_attend_selected.argtypes = [vp, u32, vp, vp, vp]

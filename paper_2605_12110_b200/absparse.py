@@ -268,6 +268,12 @@ class DecodeAttention:
     def build_store(self, layer: int, stream=None) -> None:
         check(self._lib.absp_build_store(self._ctx, layer, _stream(stream)))
 
+    def append(self, layer: int, k_new, v_new, stream=None) -> None:
+        """One token per sequence (bf16 [batch][H][d] device tensors) + store maintenance:
+        PagedKVCache::append + refresh_tail_centroids + requantize_heads (engine.cpp:443-449)."""
+        check(self._lib.absp_append(self._ctx, layer, _ptr(k_new), _ptr(v_new), _stream(stream)))
+        self._seq_lens[layer] = [n + 1 for n in self._seq_lens[layer]]
+
     # -- hot path --------------------------------------------------------------
     def select(self, layer: int, q, blocks, counts, stream=None) -> None:
         stride = int(blocks.shape[-1])
@@ -370,3 +376,90 @@ def fill_synthetic_bf16(dst, seed: int, stream_id: int, stream=None) -> None:
     """Deterministic N(0,1)-like bf16 fill on the device (same bytes as oracle/synth.py)."""
     check(_abi.load().absp_fill_synthetic_bf16(_ptr(dst), int(dst.numel()), seed, stream_id,
                                                _stream(stream)))
+
+
+def _to_bf16_bits(x) -> np.ndarray:
+    """fp32 -> bf16 bit patterns, round to nearest even (values already in bf16 stay exact)."""
+    u = np.ascontiguousarray(np.asarray(x, np.float32)).view(np.uint32).astype(np.uint64)
+    u = u + 0x7FFF + ((u >> 16) & 1)
+    return (u >> 16).astype(np.uint16)
+
+
+@dataclass
+class StepResult:
+    """StepResult (engine.hpp:84-88): output [Hq][d] fp32, selection[h] (ordered block ids)."""
+    output: np.ndarray
+    selection: list
+    full_attention_fallback: bool
+
+
+class DecodeEngine:
+    """DecodeEngine (engine.hpp:90-129, engine.cpp:405-463) on the GPU for one sequence.
+
+    Owns the paged bf16 KV cache (per-head pools, page ids handed out sequentially as
+    kv_cache.cpp:53-60 does), the quantized store, and runs prefill / step through the
+    C ABI: step = absp_append (append + refresh_tail_centroids + requantize_heads) +
+    absp_decode_step (estimate -> select -> attend). With seq_len <= token_budget every
+    block is selected, so the sparse output is the full attention the reference falls
+    back to (engine.cpp:456-458). Inputs are fp32 and stored as bf16.
+    """
+
+    def __init__(self, config: EngineConfig, assignment: BlockAssignment, capacity_tokens: int, device: int = 0):
+        import torch
+        assignment.validate(config)
+        cfg = EngineConfig(**{**config.__dict__, "max_batch": 1, "max_seq_len": int(capacity_tokens),
+                              "num_layers": 1})
+        self.config = cfg
+        self.assignment = assignment
+        self._torch = torch
+        self._dev = torch.device("cuda", device)
+        self.da = DecodeAttention(cfg, device=device)
+        self.da.set_assignment(0, assignment)
+        H, d, P = cfg.num_heads, cfg.head_dim, cfg.page_size
+        self._pages = (int(capacity_tokens) + P - 1) // P
+        self.k_pool = torch.zeros(H, self._pages, P, d, dtype=torch.int16, device=self._dev)
+        self.v_pool = torch.zeros_like(self.k_pool)
+        self.page_table = torch.arange(self._pages, dtype=torch.int32, device=self._dev).reshape(1, -1)
+        self.seq_len = 0
+        self._prefilled = False
+
+    def prefill(self, keys, values, num_tokens: int) -> None:
+        """keys / values: [H][tokens][d] fp32, the first num_tokens tokens are cached."""
+        if self._prefilled:
+            raise LogicError("prefill: engine already prefilled")
+        cfg = self.config
+        H, d, P = cfg.num_heads, cfg.head_dim, cfg.page_size
+        k = np.asarray(keys, np.float32).reshape(H, -1, d)
+        v = np.asarray(values, np.float32).reshape(H, -1, d)
+        if num_tokens == 0 or k.shape[1] < num_tokens or v.shape[1] < num_tokens:
+            raise InvalidArgument("prefill: tensor smaller than num_tokens")
+        if num_tokens > cfg.max_seq_len:
+            raise CapacityError(f"append: kv cache at capacity ({cfg.max_seq_len} tokens)")
+        pages = (num_tokens + P - 1) // P
+        for pool, src in ((self.k_pool, k), (self.v_pool, v)):
+            buf = np.zeros((H, pages * P, d), np.uint16)
+            buf[:, :num_tokens] = _to_bf16_bits(src[:, :num_tokens])
+            pool[:, :pages] = self._torch.from_numpy(buf.view(np.int16).reshape(H, pages, P, d)).to(self._dev)
+        self.da.bind(0, self.k_pool, self.v_pool, self.page_table, [num_tokens])
+        self.da.build_store(0)
+        self.seq_len = num_tokens
+        self._prefilled = True
+
+    def step(self, keys, values, query) -> StepResult:
+        """keys / values: [H][d] fp32 of the new token; query: [Hq][d] fp32."""
+        if not self._prefilled:
+            raise LogicError("step: call prefill first")
+        cfg = self.config
+        H, d = cfg.num_heads, cfg.head_dim
+        Hq = cfg.num_q_heads or H
+        torch = self._torch
+        kn = torch.from_numpy(_to_bf16_bits(np.asarray(keys).reshape(1, H, d)).view(np.int16)).to(self._dev)
+        vn = torch.from_numpy(_to_bf16_bits(np.asarray(values).reshape(1, H, d)).view(np.int16)).to(self._dev)
+        q = torch.from_numpy(_to_bf16_bits(np.asarray(query).reshape(1, Hq, d)).view(np.int16)).to(self._dev)
+        self.da.append(0, kn, vn)
+        self.seq_len += 1
+        out = torch.empty(1, Hq, d, dtype=torch.float32, device=self._dev)
+        self.da.decode_step(0, q, out)
+        torch.cuda.synchronize(self._dev)
+        sel = self.da.download_selection(0)[0]
+        return StepResult(out[0].cpu().numpy(), sel, self.seq_len <= cfg.token_budget)

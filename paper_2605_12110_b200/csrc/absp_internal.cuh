@@ -103,6 +103,9 @@ cudaError_t launch_pdl(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t sme
 
 // Launch wrappers (each returns cudaGetLastError after the launch).
 cudaError_t launch_build_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches);
+cudaError_t launch_refresh_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches);
+cudaError_t launch_append_rows(const LayerView& L, const uint16_t* k_new, const uint16_t* v_new, cudaStream_t s,
+                               int* launches);
 cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreWork& work, cudaStream_t s,
                          int* launches);
 cudaError_t init_score_attributes();  // per device, once

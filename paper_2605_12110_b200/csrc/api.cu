@@ -282,6 +282,103 @@ AttendWork work_view(const WorkList& wl) {
 
 }  // namespace
 
+// Units (capacity-reserved store segments), score work items, attention work list
+// and device buffers of a bound layer for its current seq_lens; used by kv_bind and,
+// after every sequence grew by a token, by absp_append (the store stays valid:
+// segments are reserved for max_seq_len, so no growth moves another unit's data).
+static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
+    const absp_config& c = ctx->cfg;
+    const uint32_t batch = l->batch;
+    const uint32_t* seq_lens = l->seq_lens.data();
+    absp_status st;
+    const uint32_t H = c.num_kv_heads;
+    l->desc.clear();
+    l->items.clear();
+    l->total_cap = 0;
+    l->total_centroids = 0;
+    l->max_cap = l->max_nblocks = l->max_budget = l->max_select = 0;
+    for (uint32_t b = 0; b < batch; ++b) {
+        for (uint32_t h = 0; h < H; ++h) {
+            UnitDesc d{};
+            d.seq = b;
+            d.head = h;
+            d.block = l->block_sizes[h];
+            d.n_tokens = seq_lens[b];
+            d.n_blocks = ceil_div(d.n_tokens, d.block);
+            d.budget = ceil_div(c.token_budget, d.block);
+            d.cap = ceil_div(c.max_seq_len, d.block);
+            d.seg = l->total_cap;
+            l->total_cap += d.cap;
+            l->total_centroids += d.n_blocks;
+            const uint32_t sel = std::min(d.n_blocks, d.budget);
+            l->max_cap = std::max(l->max_cap, d.cap);
+            l->max_nblocks = std::max(l->max_nblocks, d.n_blocks);
+            l->max_budget = std::max(l->max_budget, d.budget);
+            l->max_select = std::max(l->max_select, sel);
+            l->desc.push_back(d);
+        }
+    }
+    // Scoring split: CTA c gets the flattened centroid range [c*T/grid, (c+1)*T/grid),
+    // cut into per-unit items, so every CTA scores the same number of centroids
+    // whatever the block sizes (no partial last wave).
+    {
+        const uint32_t grid = uint32_t(std::max<uint64_t>(
+            1, std::min<uint64_t>(uint64_t(ctx->num_sms) * kScoreCtasPerSm, l->total_centroids)));
+        l->item_begin.assign(grid + 1, 0);
+        uint32_t u = 0;
+        uint64_t ubase = 0;  // flattened index of unit u's first centroid
+        for (uint32_t c = 0; c < grid; ++c) {
+            const uint64_t lo = l->total_centroids * c / grid, hi = l->total_centroids * (c + 1) / grid;
+            l->item_begin[c] = uint32_t(l->items.size());
+            uint64_t pos = lo;
+            while (pos < hi) {
+                while (ubase + l->desc[u].n_blocks <= pos) ubase += l->desc[u++].n_blocks;
+                const uint64_t e = std::min<uint64_t>(hi, ubase + l->desc[u].n_blocks);
+                l->items.push_back({u, uint32_t(pos - ubase), uint32_t(e - ubase), 0u});
+                pos = e;
+            }
+        }
+        l->item_begin[grid] = uint32_t(l->items.size());
+    }
+    const size_t units = l->desc.size();
+    const size_t D = c.head_dim;
+    const bool mm = c.centroid_method == ABSP_CENTROID_MAXMIN;
+    const size_t W = words_per_centroid(c);
+    ABSP_CUDA(l->d_desc.ensure(units));
+    ABSP_CUDA(l->d_items.ensure(l->items.size()));
+    ABSP_CUDA(l->d_item_begin.ensure(l->item_begin.size()));
+    ABSP_CUDA(l->values.ensure(l->total_cap * D));
+    if (mm) ABSP_CUDA(l->values_min.ensure(l->total_cap * D));
+    if (c.quant_bits) {
+        ABSP_CUDA(l->codes.ensure(l->total_cap * W));
+        ABSP_CUDA(l->scales.ensure(units * D));
+        ABSP_CUDA(l->zps.ensure(units * D));
+        if (mm) {
+            ABSP_CUDA(l->codes_min.ensure(l->total_cap * W));
+            ABSP_CUDA(l->scales_min.ensure(units * D));
+            ABSP_CUDA(l->zps_min.ensure(units * D));
+        }
+    }
+    ABSP_CUDA(l->scores.ensure(l->total_cap));
+    ABSP_CUDA(l->approx.ensure(l->total_cap));
+    ABSP_CUDA(l->unit_err.ensure(units));
+    l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
+    ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
+    ABSP_CUDA(l->sel_counts.ensure(units));
+    ABSP_CUDA(l->ready.ensure(units));
+    ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
+    for (auto& kv : l->attend_work) kv.second.release();
+    l->attend_work.clear();
+    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
+    if (st != ABSP_OK) return st;
+    ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
+                         cudaMemcpyHostToDevice));
+    ABSP_CUDA(cudaMemcpy(l->d_item_begin.p, l->item_begin.data(), l->item_begin.size() * 4,
+                         cudaMemcpyHostToDevice));
+    return ABSP_OK;
+}
+
 extern "C" {
 
 int absp_abi_version(void) { return ABSP_ABI_VERSION; }
@@ -447,92 +544,8 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
     l->batch = batch;
     l->seq_lens.assign(seq_lens, seq_lens + batch);
 
-    // Units, capacity-reserved store segments, score work items.
-    const uint32_t H = c.num_kv_heads;
-    l->desc.clear();
-    l->items.clear();
-    l->total_cap = 0;
-    l->total_centroids = 0;
-    l->max_cap = l->max_nblocks = l->max_budget = l->max_select = 0;
-    for (uint32_t b = 0; b < batch; ++b) {
-        for (uint32_t h = 0; h < H; ++h) {
-            UnitDesc d{};
-            d.seq = b;
-            d.head = h;
-            d.block = l->block_sizes[h];
-            d.n_tokens = seq_lens[b];
-            d.n_blocks = ceil_div(d.n_tokens, d.block);
-            d.budget = ceil_div(c.token_budget, d.block);
-            d.cap = ceil_div(c.max_seq_len, d.block);
-            d.seg = l->total_cap;
-            l->total_cap += d.cap;
-            l->total_centroids += d.n_blocks;
-            const uint32_t sel = std::min(d.n_blocks, d.budget);
-            l->max_cap = std::max(l->max_cap, d.cap);
-            l->max_nblocks = std::max(l->max_nblocks, d.n_blocks);
-            l->max_budget = std::max(l->max_budget, d.budget);
-            l->max_select = std::max(l->max_select, sel);
-            l->desc.push_back(d);
-        }
-    }
-    // Scoring split: CTA c gets the flattened centroid range [c*T/grid, (c+1)*T/grid),
-    // cut into per-unit items, so every CTA scores the same number of centroids
-    // whatever the block sizes (no partial last wave).
-    {
-        const uint32_t grid = uint32_t(std::max<uint64_t>(
-            1, std::min<uint64_t>(uint64_t(ctx->num_sms) * kScoreCtasPerSm, l->total_centroids)));
-        l->item_begin.assign(grid + 1, 0);
-        uint32_t u = 0;
-        uint64_t ubase = 0;  // flattened index of unit u's first centroid
-        for (uint32_t c = 0; c < grid; ++c) {
-            const uint64_t lo = l->total_centroids * c / grid, hi = l->total_centroids * (c + 1) / grid;
-            l->item_begin[c] = uint32_t(l->items.size());
-            uint64_t pos = lo;
-            while (pos < hi) {
-                while (ubase + l->desc[u].n_blocks <= pos) ubase += l->desc[u++].n_blocks;
-                const uint64_t e = std::min<uint64_t>(hi, ubase + l->desc[u].n_blocks);
-                l->items.push_back({u, uint32_t(pos - ubase), uint32_t(e - ubase), 0u});
-                pos = e;
-            }
-        }
-        l->item_begin[grid] = uint32_t(l->items.size());
-    }
-    const size_t units = l->desc.size();
-    const size_t D = c.head_dim;
-    const bool mm = c.centroid_method == ABSP_CENTROID_MAXMIN;
-    const size_t W = words_per_centroid(c);
-    ABSP_CUDA(l->d_desc.ensure(units));
-    ABSP_CUDA(l->d_items.ensure(l->items.size()));
-    ABSP_CUDA(l->d_item_begin.ensure(l->item_begin.size()));
-    ABSP_CUDA(l->values.ensure(l->total_cap * D));
-    if (mm) ABSP_CUDA(l->values_min.ensure(l->total_cap * D));
-    if (c.quant_bits) {
-        ABSP_CUDA(l->codes.ensure(l->total_cap * W));
-        ABSP_CUDA(l->scales.ensure(units * D));
-        ABSP_CUDA(l->zps.ensure(units * D));
-        if (mm) {
-            ABSP_CUDA(l->codes_min.ensure(l->total_cap * W));
-            ABSP_CUDA(l->scales_min.ensure(units * D));
-            ABSP_CUDA(l->zps_min.ensure(units * D));
-        }
-    }
-    ABSP_CUDA(l->scores.ensure(l->total_cap));
-    ABSP_CUDA(l->approx.ensure(l->total_cap));
-    ABSP_CUDA(l->unit_err.ensure(units));
-    l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
-    ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
-    ABSP_CUDA(l->sel_counts.ensure(units));
-    ABSP_CUDA(l->ready.ensure(units));
-    ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
-    for (auto& kv : l->attend_work) kv.second.release();
-    l->attend_work.clear();
-    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
+    st = layout_layer(ctx, l);
     if (st != ABSP_OK) return st;
-    ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
-                         cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(l->d_item_begin.p, l->item_begin.data(), l->item_begin.size() * 4,
-                         cudaMemcpyHostToDevice));
     l->bound = true;
     l->built = false;
     return ABSP_OK;
@@ -549,6 +562,39 @@ absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream) {
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "build_store kernels");
     l->built = true;
+    return ABSP_OK;
+}
+
+absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const void* v_new, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "step: call prefill first");  // engine.cpp:444
+    if (!k_new || !v_new) return fail(ABSP_EINVAL, "append: null pointer");
+    const absp_config& c = ctx->cfg;
+    for (uint32_t b = 0; b < l->batch; ++b) {  // kv_cache.cpp:48-50
+        if (l->seq_lens[b] >= c.max_seq_len)
+            return fail(ABSP_ECAPACITY, "append: kv cache at capacity (" + std::to_string(c.max_seq_len) + " tokens)");
+        if (l->seq_lens[b] >= uint64_t(l->max_pages) * c.page_size)
+            return fail(ABSP_ECAPACITY, "append: page table of sequence " + std::to_string(b) + " is full");
+    }
+    DeviceGuard dg(ctx->device);
+    const cudaStream_t s = cudaStream_t(stream);
+    int n = 0;
+    cudaError_t e = launch_append_rows(view_of(ctx, *l), static_cast<const uint16_t*>(k_new),
+                                       static_cast<const uint16_t*>(v_new), s, &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "append kernel");
+    ABSP_CUDA(cudaStreamSynchronize(s));  // the unit layout below is rewritten synchronously
+    for (uint32_t b = 0; b < l->batch; ++b) ++l->seq_lens[b];
+    l->drop_host_graph();
+    st = layout_layer(ctx, l);
+    if (st != ABSP_OK) return st;
+    n = 0;
+    e = launch_refresh_store(view_of(ctx, *l), l->max_cap, s, &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "refresh_store kernels");
+    l->selected = false;
     return ABSP_OK;
 }
 

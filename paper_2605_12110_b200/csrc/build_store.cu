@@ -148,13 +148,73 @@ __global__ void __launch_bounds__(32 * (D * BITS / 32)) k_encode(LayerView L, co
     codes[(du.seg + i) * W + code_word_pos(i, w, W)] = word;
 }
 
+// Decode-time append (PagedKVCache::append, kv_cache.cpp:44-70): token n of
+// sequence b goes to row n % P of page page_table[b][n / P] of every KV head.
+// One CTA per unit (b, h), one thread per channel; n is the unit's n_tokens
+// before the append.
+__global__ void k_append_rows(LayerView L, const uint16_t* __restrict__ k_new, const uint16_t* __restrict__ v_new,
+                              uint16_t* k_pool, uint16_t* v_pool) {
+    const uint32_t u = blockIdx.x;
+    const UnitDesc du = L.desc[u];
+    const uint32_t n = du.n_tokens;
+    const uint32_t page = L.page_table[size_t(du.seq) * L.max_pages + n / L.P];
+    const size_t row = ((size_t(du.head) * L.pool_pages + page) * L.P + n % L.P) * L.D;
+    const size_t src = (size_t(du.seq) * L.H + du.head) * L.D;
+    for (uint32_t c = threadIdx.x; c < L.D; c += blockDim.x) {
+        k_pool[row + c] = k_new[src + c];
+        v_pool[row + c] = v_new[src + c];
+    }
+}
+
+// refresh_tail_centroid (centroids.cpp:122-156): after one appended token only the
+// trailing block of a unit changed (the previous partial tail, or a block that just
+// started); it is recomputed exactly like k_centroids. One CTA per unit.
+template <int D, int METHOD>
+__global__ void __launch_bounds__(D) k_tail_centroid(LayerView L) {
+    const uint32_t u = blockIdx.x;
+    const UnitDesc du = L.desc[u];
+    const uint32_t c = threadIdx.x;
+    const uint32_t i = du.n_blocks - 1;
+    const uint32_t begin = i * du.block;
+    const uint32_t end = min(begin + du.block, du.n_tokens);
+    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+    const size_t head_base = size_t(du.head) * L.pool_pages;
+    const size_t out = (du.seg + i) * D + c;
+    if (METHOD == ABSP_CENTROID_MEAN) {
+        double acc = 0.0;
+        for (uint32_t t = begin; t < end; ++t) {
+            const size_t row = ((head_base + pt[t / L.P]) * L.P + t % L.P) * D;
+            acc = __dadd_rn(acc, double(bf16f(L.k_pool[row + c])));
+        }
+        const double inv = __ddiv_rn(1.0, double(end - begin));
+        L.values[out] = __double2float_rn(__dmul_rn(acc, inv));
+    } else {
+        float hi = -INFINITY, lo = INFINITY;
+        for (uint32_t t = begin; t < end; ++t) {
+            const size_t row = ((head_base + pt[t / L.P]) * L.P + t % L.P) * D;
+            const float v = bf16f(L.k_pool[row + c]);
+            hi = (hi < v) ? v : hi;
+            lo = (v < lo) ? v : lo;
+        }
+        L.values[out] = hi;
+        L.values_min[out] = lo;
+    }
+}
+
 template <int D>
-cudaError_t build_d(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches) {
-    const dim3 gc((max_cap + 7) / 8, L.units);
-    if (L.method == ABSP_CENTROID_MEAN)
-        k_centroids<D, ABSP_CENTROID_MEAN><<<gc, D * 8, 0, s>>>(L);
-    else
-        k_centroids<D, ABSP_CENTROID_MAXMIN><<<gc, D * 8, 0, s>>>(L);
+cudaError_t build_d(const LayerView& L, uint32_t max_cap, bool tail_only, cudaStream_t s, int* launches) {
+    if (tail_only) {  // decode-time maintenance: only each unit's trailing block changed
+        if (L.method == ABSP_CENTROID_MEAN)
+            k_tail_centroid<D, ABSP_CENTROID_MEAN><<<L.units, D, 0, s>>>(L);
+        else
+            k_tail_centroid<D, ABSP_CENTROID_MAXMIN><<<L.units, D, 0, s>>>(L);
+    } else {
+        const dim3 gc((max_cap + 7) / 8, L.units);
+        if (L.method == ABSP_CENTROID_MEAN)
+            k_centroids<D, ABSP_CENTROID_MEAN><<<gc, D * 8, 0, s>>>(L);
+        else
+            k_centroids<D, ABSP_CENTROID_MAXMIN><<<gc, D * 8, 0, s>>>(L);
+    }
     ++*launches;
     if (L.bits == 0) return cudaGetLastError();
     const int arrays = L.method == ABSP_CENTROID_MAXMIN ? 2 : 1;
@@ -179,8 +239,25 @@ cudaError_t build_d(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* l
 }  // namespace
 
 cudaError_t launch_build_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches) {
-    if (L.D == 64) return build_d<64>(L, max_cap, s, launches);
-    return build_d<128>(L, max_cap, s, launches);
+    if (L.D == 64) return build_d<64>(L, max_cap, false, s, launches);
+    return build_d<128>(L, max_cap, false, s, launches);
+}
+
+// DecodeEngine::step's maintenance after an append (engine.cpp:445-449):
+// refresh_tail_centroids, then requantize_heads over every head — per-(unit,
+// channel) parameters from all centroids and every code re-encoded, which is
+// exactly what quantizing the grown store from scratch gives.
+cudaError_t launch_refresh_store(const LayerView& L, uint32_t max_cap, cudaStream_t s, int* launches) {
+    if (L.D == 64) return build_d<64>(L, max_cap, true, s, launches);
+    return build_d<128>(L, max_cap, true, s, launches);
+}
+
+cudaError_t launch_append_rows(const LayerView& L, const uint16_t* k_new, const uint16_t* v_new, cudaStream_t s,
+                               int* launches) {
+    k_append_rows<<<L.units, 128, 0, s>>>(L, k_new, v_new, const_cast<uint16_t*>(L.k_pool),
+                                          const_cast<uint16_t*>(L.v_pool));
+    ++*launches;
+    return cudaGetLastError();
 }
 
 }  // namespace absp
