@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 gp[k] = f0.gp[k];
                 vl[k] = f0.vl[k];
             }
+            f0 = f1;
+            fetch(w + 2, f1);  // its loads fly while this chunk waits for a free stage
             mbar_wait(smem_u32(&sh.empty[stage]), phase ^ 1);
             StageMeta& mt = sh.meta[stage];
             const uint32_t kdst = smem_base + stage * 2 * TB;
@@ -259,9 +261,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 stage = 0;
                 phase ^= 1;
             }
-            // chunk w+2's page list: after the issue, so a flag wait never delays chunk w
-            f0 = f1;
-            fetch(w + 2, f1);
         }
         return;
     }
