@@ -195,6 +195,17 @@ def run_reference(args, w, rank, world):
 # ---------------------------------------------------------------------------
 # B200 path
 # ---------------------------------------------------------------------------
+def measured_traffic(workload):
+    """DRAM read+write bytes of one k_attn launch from the committed ncu capture
+    (profiles/r1/attn_traffic.json) when it is of this workload, else None."""
+    f = ROOT / "profiles" / "r1" / "attn_traffic.json"
+    try:
+        t = json.loads(f.read_text())
+    except (OSError, ValueError):
+        return None
+    return t["dram_bytes_read"] + t["dram_bytes_write"] if t.get("workload") == workload else None
+
+
 def trace(msg):
     if os.environ.get("ABSP_BENCH_TRACE"):
         print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
@@ -365,7 +376,8 @@ def run_absp(args, w, rank, world, local):
                        "compute": "int4 codes -> exact fp32 scores; bf16 MMA (mma.sync) fp32 accumulate"},
             "roofline": {"bound": "hbm", "kernel": "k_attn (absp_attend_selected: paged flash-decode + fused LSE merge)",
                          "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
-                         "traffic": None, "bytes_per_launch": attn_bytes, "peak_source": peak_src},
+                         "traffic": measured_traffic(args.workload), "bytes_per_launch": attn_bytes,
+                         "peak_source": peak_src},
             "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms_step / 1e3) / 1e9,
                               "frac": step_bytes / (ms_step / 1e3) / 1e9 / peak},
             "kernels_us": {"step": ms_step * 1e3, "select": ms_sel * 1e3, "attend": ms_attn * 1e3,
