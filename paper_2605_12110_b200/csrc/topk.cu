@@ -225,34 +225,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) C += sm.red[0][w];
         if (C >= K1 && C <= uint32_t(kMaxSort)) {
-            // compact the candidates as composite keys (key << 32 | ~index)
+            // compact the candidates as composite keys (key << 32 | ~index): each warp
+            // writes at its prefix of the per-warp counts, no atomics
+            uint32_t pos = 0;
+            for (uint32_t w = 0; w < warp; ++w) pos += sm.red[0][w];
 #pragma unroll
             for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = (j * kWarps + warp) * 32 + lane;
                 const bool in = i < n_cand && keys.r[j] >= x;
                 const uint32_t m = __ballot_sync(0xffffffffu, in);
-                if (m) {
-                    uint32_t base = 0;
-                    if (lane == 0) base = atomicAdd(&sm.state[4], __popc(m));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (in) sm.sel[base + __popc(m & ((1u << lane) - 1u))] = (uint64_t(keys.r[j]) << 32) | uint32_t(~i);
-                }
+                if (in) sm.sel[pos + __popc(m & ((1u << lane) - 1u))] = (uint64_t(keys.r[j]) << 32) | uint32_t(~i);
+                pos += __popc(m);
             }
             __syncthreads();
             TOPK_TRACE(3);
             const unsigned long long ct = (uint64_t(order_key(tail_score)) << 32) | uint32_t(~(N - 1));
             uint32_t* out = sm.outs;
             if (C <= 256) {
-                // rank among candidates = output position (composites are distinct)
-                for (uint32_t p = threadIdx.x; p < C; p += kThreads) {
-                    const unsigned long long me = sm.sel[p];
-                    uint32_t rank = 0;
-                    for (uint32_t o = 0; o < C; ++o) rank += sm.sel[o] > me;
-                    if (rank < K1) {
-                        out[rank + (ct > me ? 1u : 0u)] = ~uint32_t(me);
-                        if (me > ct) atomicAdd(&sm.nsel, 1u);
-                    }
+                // rank among candidates = output position (composites are distinct);
+                // tpc adjacent lanes share a candidate, each counting a strided share
+                const uint32_t tpc = C <= 128 ? 4u : 2u;
+                const uint32_t t = threadIdx.x, j = t / tpc, part = t % tpc;
+                const bool valid = j < C;
+                const unsigned long long me = valid ? sm.sel[j] : 0ull;
+                uint32_t rank = 0;
+                if (valid)
+                    for (uint32_t o = part; o < C; o += tpc) rank += sm.sel[o] > me;
+                for (uint32_t off = 1; off < tpc; off <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
+                bool above = false;  // a winner ranked before the trailing block
+                if (valid && part == 0 && rank < K1) {
+                    out[rank + (ct > me ? 1u : 0u)] = ~uint32_t(me);
+                    above = me > ct;
                 }
+                const uint32_t n_above = __syncthreads_count(above);
+                if (threadIdx.x == 0) sm.nsel = n_above;
             } else {
                 uint32_t sp = 1;
                 while (sp < C) sp <<= 1;
