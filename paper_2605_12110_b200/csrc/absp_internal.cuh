@@ -40,6 +40,8 @@ struct ScoreWork {
     const ScoreItem* items;
     const uint32_t* item_begin;  // [grid + 1]
     uint32_t grid;
+    uint32_t* scored;            // [units] centroids scored this step (table scorer; null: none),
+                                 // lets the top-k of a unit start before the whole grid ends
 };
 
 // Everything a kernel needs about one bound layer.
@@ -122,9 +124,11 @@ struct PageList {
 // ready (decode step, else null): per-unit "selection published" flags, raised by the
 // selection kernel after the unit's blocks and page list are written (release) and
 // re-armed by the attention merge; the attention producer starts a unit on its flag.
+// scored (else null): the scorer's per-unit completion counters (ScoreWork::scored);
+// a unit's top-k starts once its count reaches N and re-arms it.
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                        uint32_t* ready, cudaStream_t s, int* launches);
+                        uint32_t* ready, uint32_t* scored, cudaStream_t s, int* launches);
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
                                  const uint32_t* counts, const PageList& pages, cudaStream_t s,
                                  int* launches);

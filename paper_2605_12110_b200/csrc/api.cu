@@ -116,7 +116,8 @@ struct Layer {
     DevBuf<float> values, values_min, scales, zps, scales_min, zps_min, scores;
     DevBuf<uint32_t> codes, codes_min;
     DevBuf<uint32_t> sel_blocks, sel_counts;
-    DevBuf<uint32_t> ready;  // decode step: per-unit "selection published" flags (zero between steps)
+    DevBuf<uint32_t> ready;   // decode step: per-unit "selection published" flags (zero between steps)
+    DevBuf<uint32_t> scored;  // per-unit scored-centroid counters (zero between steps)
     DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
     DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
@@ -143,7 +144,7 @@ struct Layer {
         values.release(); values_min.release(); scales.release(); zps.release();
         scales_min.release(); zps_min.release(); scores.release();
         codes.release(); codes_min.release();
-        sel_blocks.release(); sel_counts.release(); ready.release();
+        sel_blocks.release(); sel_counts.release(); ready.release(); scored.release();
         approx.release(); unit_err.release();
         part_o.release(); part_ml.release();
         stage_q.release(); stage_out.release();
@@ -367,6 +368,8 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
     ABSP_CUDA(l->sel_counts.ensure(units));
     ABSP_CUDA(l->ready.ensure(units));
     ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
+    ABSP_CUDA(l->scored.ensure(units));
+    ABSP_CUDA(cudaMemset(l->scored.p, 0, units * 4));
     for (auto& kv : l->attend_work) kv.second.release();
     l->attend_work.clear();
     st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
@@ -606,10 +609,13 @@ static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* b
                              uint32_t* counts, uint32_t* ready, cudaStream_t s) {
     const LayerView v = view_of(ctx, *l);
     int n = 0;
-    const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1)};
+    // the table scorer publishes per-unit progress, so each unit's top-k starts on it
+    uint32_t* scored = (v.bits == 2 || v.bits == 4) ? l->scored.p : nullptr;
+    const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1), scored};
     cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), sw, s, &n);
     if (e == cudaSuccess)
-        e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), ready, s, &n);
+        e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), ready, scored,
+                        s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "select kernels");
     return ABSP_OK;
@@ -694,7 +700,7 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     const cudaStream_t s = cudaStream_t(stream);
     const LayerView v = view_of(ctx, *l);
     if (ctx->fast_select && select_fast_supported(v, l->max_nblocks, l->max_budget)) {
-        const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1)};
+        const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1), nullptr};
         int n = 0;
         cudaError_t e = launch_select_fast(v, static_cast<const uint16_t*>(q), sw, l->approx.p, l->unit_err.p,
                                            l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->step_work.pages(),

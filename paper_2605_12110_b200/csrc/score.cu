@@ -170,7 +170,23 @@ __global__ void __launch_bounds__(kTblThreads, kScoreCtasPerSm) k_score_tbl(Laye
 
     if (warp == kConsumerWarps) {
         // ================================ producer ================================
+        // Besides the copies, the producer publishes progress: when the last chunk of
+        // an item has been consumed (its stage released by every consumer warp, after
+        // their score stores), the item's centroids are added to scored[unit] behind a
+        // fence, so the top-k of a unit can start as soon as its last item is done.
         if (lane != 0) return;
+        uint32_t pub_unit[NS], pub_len[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) pub_len[i] = 0u;
+        auto publish = [&](uint32_t st) {
+#pragma unroll
+            for (int i = 0; i < NS; ++i)
+                if (uint32_t(i) == st && pub_len[i]) {
+                    __threadfence();
+                    atomicAdd(work.scored + pub_unit[i], pub_len[i]);
+                    pub_len[i] = 0u;
+                }
+        };
         uint32_t chunk = 0;
         ScoreItem nxt = work.items[it0];
         for (uint32_t k = it0; k < it1; ++k) {
@@ -196,7 +212,10 @@ __global__ void __launch_bounds__(kTblThreads, kScoreCtasPerSm) k_score_tbl(Laye
             }
             for (uint32_t pos = it.start; pos < it.end; pos += kChunkRows, ++chunk) {
                 const uint32_t st = chunk % NS;
-                if (chunk >= uint32_t(NS)) mbar_wait(smem_u32(&bars[NS + st]), ((chunk / NS) - 1) & 1);
+                if (chunk >= uint32_t(NS)) {
+                    mbar_wait(smem_u32(&bars[NS + st]), ((chunk / NS) - 1) & 1);
+                    if (work.scored) publish(st);
+                }
                 const uint32_t n = min(uint32_t(kChunkRows), it.end - pos);
                 const uint32_t bar = smem_u32(&bars[st]);
                 mbar_expect_tx(bar, NT * n * C::ROWB);
@@ -204,8 +223,19 @@ __global__ void __launch_bounds__(kTblThreads, kScoreCtasPerSm) k_score_tbl(Laye
                 if (MAXMIN)
                     bulk_g2s(smem_u32(ring + size_t(st * NT + 1) * C::STAGEB), L.codes_min + (seg + pos) * W,
                              n * C::ROWB, bar);
+#pragma unroll
+                for (int i = 0; i < NS; ++i)
+                    if (uint32_t(i) == st) {
+                        pub_unit[i] = u;
+                        pub_len[i] = pos + n >= it.end ? it.end - it.start : 0u;
+                    }
             }
         }
+        if (work.scored)  // the chunks still in flight
+            for (uint32_t j = chunk > uint32_t(NS) ? chunk - NS : 0u; j < chunk; ++j) {
+                mbar_wait(smem_u32(&bars[NS + j % NS]), (j / NS) & 1);
+                publish(j % NS);
+            }
         return;
     }
 

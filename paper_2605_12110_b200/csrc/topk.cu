@@ -81,6 +81,12 @@ struct Keys {
 };
 
 // One radix pass over a warp-step's 32 keys: adds this lane's bin count.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t prefix, uint32_t pmask,
                                               int shift, int nbits, const uint32_t* xm) {
     const uint32_t m = __ballot_sync(0xffffffffu, in && (key & pmask) == prefix);
@@ -94,7 +100,8 @@ __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t pr
 
 template <bool REG, int ITEMS>
 __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
-                                                   uint32_t* counts, PageList pages, uint32_t* ready) {
+                                                   uint32_t* counts, PageList pages, uint32_t* ready,
+                                                   uint32_t* scored) {
     __shared__ TopkSmem sm;
     TOPK_TRACE(0);
     const uint32_t u = blockIdx.x;
@@ -109,7 +116,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     const int my_items = REG ? ITEMS : int((nsteps + kWarps - 1 - warp) / kWarps);
 
     griddep_launch_dependents();
-    griddep_wait();  // the scores are written by the scoring kernel of this step
+    if (scored) {
+        // the unit's scores are complete once the scorer's producers have published all
+        // N of them (release); then re-arm the counter for the next step
+        if (threadIdx.x == 0) {
+            while (ld_acquire(scored + u) < N) __nanosleep(64);
+            scored[u] = 0u;
+        }
+        __syncthreads();
+    } else {
+        griddep_wait();  // the scores are written by the scoring kernel of this step
+    }
     const float tail_score = N > K ? __ldg(sc + N - 1) : 0.0f;  // the trailing block, loaded early
     Keys<REG, ITEMS> keys;
     keys.sc = sc;
@@ -553,13 +570,13 @@ cudaError_t debug_topk_trace(void* dst, size_t bytes) {
 
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                        uint32_t* ready,
+                        uint32_t* ready, uint32_t* scored,
                         cudaStream_t s, int* launches) {
     if (max_budget > uint32_t(kMaxSort) || max_nblocks > uint32_t(kMaxSteps) * 32u)
         return cudaErrorInvalidValue;
     const uint32_t per_thread = (max_nblocks + kThreads - 1) / kThreads;
     const dim3 grid(L.units);
-#define ABSP_TOPK(REG, IT) launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages, ready)
+#define ABSP_TOPK(REG, IT) launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages, ready, scored)
     if (per_thread <= 1) ABSP_TOPK(true, 1);
     else if (per_thread <= 2) ABSP_TOPK(true, 2);
     else if (per_thread <= 4) ABSP_TOPK(true, 4);

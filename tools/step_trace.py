@@ -64,6 +64,10 @@ for rep in range(2):
     print(f"  scorer end        {pct(r(sc[:ns, 1]))}")
     if tk[:units, 0].max() >= sc[:ns, 0].min():
         print(f"  topk start        {pct(r(tk[:units, 0]))}")
+        for j, nm in ((1, "topk keys issued"), (2, "topk threshold"), (3, "topk compacted"), (4, "topk ordered")):
+            v = tk[:units, j]
+            if (v > 0).any():
+                print(f"  {nm:17s} {pct(r(v[v > 0]))}")
         print(f"  topk end (pages)  {pct(r(tk[:units, 5][tk[:units, 5] > 0]))}")
     print(f"  attn CTA start    {pct(r(at[:148, 0]))}")
     if at[:148, 250].max() > 0:
