@@ -14,9 +14,13 @@ mirror the reference's C++ exception classes:
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libabsp.so"
+# ABSP_LIB=<file name in lib/> loads another build of the same ABI (A/B measurements)
+if os.environ.get("ABSP_LIB"):
+    LIB_PATH = LIB_PATH.with_name(os.path.basename(os.environ["ABSP_LIB"]))
 
 ABSP_MAX_CANDIDATES = 16
 

@@ -56,8 +56,7 @@ constexpr int kStages = 3;
 constexpr int kWarpRows = kRows / kWarps;  // 16
 constexpr int kPStride = kWarpRows + 8;    // bf16 row stride of a P tile (bank-conflict free)
 constexpr int kMaxSlots = kRows;           // P >= 1
-constexpr int kMaxDone = 32;               // runs whose completion a CTA counts after its loop
-constexpr int kMaxPend = 2 * kMaxDone;     // unit merges deferred to after the loop
+constexpr int kMaxPend = 32;               // units completed by one CTA
 
 // Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
 // globaltimer stamps of the producer's issues, warp 0's data arrivals / releases,
@@ -133,8 +132,6 @@ struct SmemHead {  // fixed-size part after the stage tiles
     StageMeta meta[kStages];
     uint32_t npend;          // units this CTA completed (merged after the chunk loop)
     uint32_t pend[kMaxPend];
-    uint32_t done_unit[kMaxDone];    // runs flushed by this CTA, counted after the loop
-    uint32_t done_chunks[kMaxDone];
     uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
 };
 
@@ -376,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count its
     // chunks; no barrier with the other warps. The warp completing a unit queues its
     // merge, done by the CTA's warps after the chunk loop.
-    auto flush = [&](uint32_t k) {
+    auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
@@ -403,30 +400,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             ml[(2 * t4 + 1) * 2] = m_run[1];
             ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
         }
-        // Completion counting is deferred to after the chunk loop: a release here
-        // (a gpu-scope fence behind this warp's partial stores) stalls the warp for
-        // microseconds under full HBM load, and with it the stage ring. Every warp
-        // flushes the same run sequence, so warp 0 records run k; the CTA counts them
-        // after its loop behind one barrier + fence. Past kMaxDone runs (many tiny
-        // units per CTA) each warp counts its own chunks right away.
-        const uint32_t mine = seg_last - seg_first + 1;
-        if (k < uint32_t(kMaxDone)) {
-            if (warp == 0 && lane == 0) {
-                sh.done_unit[k] = cur_u;
-                sh.done_chunks[k] = mine;
-            }
-            return;
-        }
+        // completion counting: the release publishes this warp's partials to the warp
+        // that completes the unit, whose acquire makes every partial visible to it
         __syncwarp();
         uint32_t merge_now = 0;
         if (lane == 0) {
             const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
+            const uint32_t mine = seg_last - seg_first + 1;
             const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
             if (done == kWarps * nch) {
                 unit_done[cur_u] = 0u;  // re-arm for the next step
                 const uint32_t slot_p = atomicAdd(&sh.npend, 1u);
-                if (slot_p < uint32_t(kMaxPend - kMaxDone)) sh.pend[slot_p] = cur_u;
-                else merge_now = 1u;  // keep room for the deferred runs: merge right away
+                if (slot_p < uint32_t(kMaxPend)) sh.pend[slot_p] = cur_u;
+                else merge_now = 1u;  // queue full: this warp merges right away
             }
         }
         if (__shfl_sync(0xffffffffu, merge_now, 0))
@@ -434,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     };
 
     uint32_t stage = 0, phase = 0, nflush = 0;
+    (void)nflush;
     for (uint32_t w = w_begin; w < w_end; ++w) {
         mbar_wait(smem_u32(&sh.full[stage]), phase);
         if (tid == 0) ATTN_TRACE(64 + (w - w_begin));  // data arrived (warp 0)
@@ -499,8 +486,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 
         if (new_unit) {
             if (tid == 0) ATTN_TRACE(192 + 2 * (nflush & 3));
-            if (cur_u != 0xffffffffu) flush(nflush++);
+            if (cur_u != 0xffffffffu) flush();
             if (tid == 0) ATTN_TRACE(193 + 2 * (nflush & 3));
+            ++nflush;
             cur_u = u;
             seg_first = chunk;
             m_run[0] = m_run[1] = -INFINITY;
@@ -557,23 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
     }
     if (tid == 0) ATTN_TRACE(240);
-    if (cur_u != 0xffffffffu) flush(nflush++);
+    if (cur_u != 0xffffffffu) flush();
     if (tid == 0) ATTN_TRACE(241);
-    consumer_sync();
-    // count the recorded runs: the barrier orders every warp's partial stores before
-    // warp 0's fence; then one atomic per run from the lanes, in parallel
-    if (warp == 0) {
-        __threadfence();
-        const uint32_t nrec = min(nflush, uint32_t(kMaxDone));
-        if (lane < nrec) {
-            const uint32_t u = sh.done_unit[lane], c = sh.done_chunks[lane] * kWarps;
-            const uint32_t nch = chunk_base[u + 1] - chunk_base[u];
-            if (atom_add_acq_rel(unit_done + u, c) + c == kWarps * nch) {
-                unit_done[u] = 0u;  // re-arm for the next step
-                sh.pend[atomicAdd(&sh.npend, 1u)] = u;  // <= kMaxPend: see flush
-            }
-        }
-    }
     consumer_sync();
     // pending merges: warp w takes (unit, head) pairs w, w + 8, ...
     const uint32_t npend = min(sh.npend, uint32_t(kMaxPend));
