@@ -124,11 +124,22 @@ struct PageList {
 // ready (decode step, else null): per-unit "selection published" flags, raised by the
 // selection kernel after the unit's blocks and page list are written (release) and
 // re-armed by the attention merge; the attention producer starts a unit on its flag.
+// Top-k launch classes: units grouped by the register variant their block count
+// needs (topk_items), so a layer with mixed block sizes does not run every unit with
+// the keys-per-thread of its largest one. units = null: one launch.
+constexpr int kTopkClasses = 8;
+struct TopkClasses {
+    const uint32_t* units;           // [units] grouped by class
+    uint32_t begin[kTopkClasses + 1];
+    uint32_t items[kTopkClasses];    // keys per thread of each class (0: L2-resident keys)
+};
+uint32_t topk_items(uint32_t n_blocks);
 // scored (else null): the scorer's per-unit completion counters (ScoreWork::scored);
 // a unit's top-k starts once its count reaches N and re-arms it.
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                        uint32_t* ready, uint32_t* scored, cudaStream_t s, int* launches);
+                        uint32_t* ready, uint32_t* scored, const TopkClasses& classes, cudaStream_t s,
+                        int* launches);
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
                                  const uint32_t* counts, const PageList& pages, cudaStream_t s,
                                  int* launches);

@@ -118,6 +118,8 @@ struct Layer {
     DevBuf<uint32_t> sel_blocks, sel_counts;
     DevBuf<uint32_t> ready;   // decode step: per-unit "selection published" flags (zero between steps)
     DevBuf<uint32_t> scored;  // per-unit scored-centroid counters (zero between steps)
+    DevBuf<uint32_t> topk_units;  // units grouped by top-k register class
+    TopkClasses topk_classes{};
     DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
     DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
@@ -144,7 +146,7 @@ struct Layer {
         values.release(); values_min.release(); scales.release(); zps.release();
         scales_min.release(); zps_min.release(); scores.release();
         codes.release(); codes_min.release();
-        sel_blocks.release(); sel_counts.release(); ready.release(); scored.release();
+        sel_blocks.release(); sel_counts.release(); ready.release(); scored.release(); topk_units.release();
         approx.release(); unit_err.release();
         part_o.release(); part_ml.release();
         stage_q.release(); stage_out.release();
@@ -370,6 +372,22 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
     ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
     ABSP_CUDA(l->scored.ensure(units));
     ABSP_CUDA(cudaMemset(l->scored.p, 0, units * 4));
+    // top-k classes: split only when the largest unit needs the big register variants
+    l->topk_classes = TopkClasses{};
+    if (topk_items(l->max_nblocks) >= 32 || topk_items(l->max_nblocks) == 0) {
+        static const uint32_t kItems[kTopkClasses] = {0, 64, 32, 16, 8, 4, 2, 1};  // largest first
+        std::vector<uint32_t> order;
+        for (int cls = 0; cls < kTopkClasses; ++cls) {
+            l->topk_classes.items[cls] = kItems[cls];
+            l->topk_classes.begin[cls] = uint32_t(order.size());
+            for (uint32_t u = 0; u < units; ++u)
+                if (topk_items(l->desc[u].n_blocks) == kItems[cls]) order.push_back(u);
+        }
+        l->topk_classes.begin[kTopkClasses] = uint32_t(order.size());
+        ABSP_CUDA(l->topk_units.ensure(units));
+        ABSP_CUDA(cudaMemcpy(l->topk_units.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
+        l->topk_classes.units = l->topk_units.p;
+    }
     for (auto& kv : l->attend_work) kv.second.release();
     l->attend_work.clear();
     st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
@@ -615,7 +633,7 @@ static absp_status do_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* b
     cudaError_t e = launch_score(v, static_cast<const uint16_t*>(q), sw, s, &n);
     if (e == cudaSuccess)
         e = launch_topk(v, l->max_nblocks, l->max_budget, blocks, stride, counts, l->step_work.pages(), ready, scored,
-                        s, &n);
+                        l->topk_classes, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "select kernels");
     return ABSP_OK;

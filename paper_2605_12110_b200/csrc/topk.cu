@@ -101,10 +101,10 @@ __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t pr
 template <bool REG, int ITEMS>
 __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
                                                    uint32_t* counts, PageList pages, uint32_t* ready,
-                                                   uint32_t* scored) {
+                                                   uint32_t* scored, const uint32_t* __restrict__ unit_list) {
     __shared__ TopkSmem sm;
     TOPK_TRACE(0);
-    const uint32_t u = blockIdx.x;
+    const uint32_t u = unit_list ? unit_list[blockIdx.x] : blockIdx.x;
     const UnitDesc du = L.desc[u];
     const uint32_t N = du.n_blocks;
     const uint32_t K = du.budget;
@@ -568,25 +568,59 @@ cudaError_t debug_topk_trace(void* dst, size_t bytes) {
 }
 #endif
 
+// Keys per thread of the register-resident variant for a unit of n blocks (0: too
+// many for registers, keys re-read from L2).
+uint32_t topk_items(uint32_t n_blocks) {
+    const uint32_t per_thread = (n_blocks + kThreads - 1) / kThreads;
+    for (uint32_t it = 1; it <= 64; it <<= 1)
+        if (per_thread <= it) return it;
+    return 0;
+}
+
+template <bool REG, int IT>
+cudaError_t topk_launch(const LayerView& L, uint32_t grid, uint32_t* blocks, uint32_t stride, uint32_t* counts,
+                        const PageList& pages, uint32_t* ready, uint32_t* scored, const uint32_t* unit_list,
+                        cudaStream_t s) {
+    return launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages, ready,
+                      scored, unit_list);
+}
+
+cudaError_t launch_topk_class(const LayerView& L, uint32_t items, uint32_t grid, uint32_t* blocks, uint32_t stride,
+                              uint32_t* counts, const PageList& pages, uint32_t* ready, uint32_t* scored,
+                              const uint32_t* unit_list, cudaStream_t s) {
+    switch (items) {
+        case 1: return topk_launch<true, 1>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 2: return topk_launch<true, 2>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 4: return topk_launch<true, 4>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 8: return topk_launch<true, 8>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 16: return topk_launch<true, 16>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 32: return topk_launch<true, 32>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 64: return topk_launch<true, 64>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        default: return topk_launch<false, 1>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+    }
+}
+
 cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget,
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                        uint32_t* ready, uint32_t* scored,
+                        uint32_t* ready, uint32_t* scored, const TopkClasses& classes,
                         cudaStream_t s, int* launches) {
     if (max_budget > uint32_t(kMaxSort) || max_nblocks > uint32_t(kMaxSteps) * 32u)
         return cudaErrorInvalidValue;
-    const uint32_t per_thread = (max_nblocks + kThreads - 1) / kThreads;
-    const dim3 grid(L.units);
-#define ABSP_TOPK(REG, IT) launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages, ready, scored)
-    if (per_thread <= 1) ABSP_TOPK(true, 1);
-    else if (per_thread <= 2) ABSP_TOPK(true, 2);
-    else if (per_thread <= 4) ABSP_TOPK(true, 4);
-    else if (per_thread <= 8) ABSP_TOPK(true, 8);
-    else if (per_thread <= 16) ABSP_TOPK(true, 16);
-    else if (per_thread <= 32) ABSP_TOPK(true, 32);
-    else if (per_thread <= 64) ABSP_TOPK(true, 64);
-    else ABSP_TOPK(false, 1);
-#undef ABSP_TOPK
-    ++*launches;
+    if (!classes.units) {  // one launch sized for the largest unit
+        ++*launches;
+        cudaError_t e = launch_topk_class(L, topk_items(max_nblocks), L.units, blocks, stride, counts, pages, ready,
+                                          scored, nullptr, s);
+        return e == cudaSuccess ? cudaGetLastError() : e;
+    }
+    // one launch per register class, units grouped by class (largest first)
+    for (int c = 0; c < kTopkClasses; ++c) {
+        const uint32_t n = classes.begin[c + 1] - classes.begin[c];
+        if (n == 0) continue;
+        ++*launches;
+        cudaError_t e = launch_topk_class(L, classes.items[c], n, blocks, stride, counts, pages, ready, scored,
+                                          classes.units + classes.begin[c], s);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 

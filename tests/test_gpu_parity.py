@@ -167,6 +167,24 @@ def test_filter_error_bound(cuda):
                 assert err[h] < 0.05 * (e.max() - e.min()), (scale, b, h, err[h])
 
 
+def test_topk_register_classes(cuda):
+    """Block sizes 4..64 on a 70K-token sequence: units of 17,500 down to 1,094 blocks run as
+    separate top-k register classes (64 keys per thread down to 4); selections and outputs
+    against the oracle."""
+    from gpu_util import GpuLayer, within_tol
+    layer = make_layer(77, H=5, G=2, d=128, P=4, block_sizes=(4, 8, 16, 32, 64), seq_lens=(70000, 30000))
+    gl = GpuLayer(layer, 2048)
+    sel = gl.select()
+    out = gl.decode()
+    for b in range(layer.batch):
+        _, _, want_sel, want = oracle_step(layer, b, 2048)
+        for h in range(layer.H):
+            assert np.array_equal(sel[b][h], want_sel[h]), (b, h)
+            assert np.array_equal(gl.step_selection[b][h], want_sel[h]), ("decode step", b, h)
+        ok, err = within_tol(out[b], want)
+        assert ok, f"seq {b}: max abs err {err}"
+
+
 @pytest.mark.parametrize("fast", [False, True])
 def test_decode_step_selection_many_seeds(cuda, fast):
     """The decode step's selection (exact scorer + top-k, or select.cu's filter + exact
