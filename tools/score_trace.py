@@ -59,7 +59,11 @@ for rep in range(3):
     print(f"  first table {pct(ft)}")
     print(f"  end         {pct(en)}")
     print(f"  busy        {pct(en - st)}")
-    smid_end = en
+    nitems = np.array([sum(1 for i in range(14) if tr[c, 2 + i] and int(tr[c, 2 + i]) >= int(tr[c, 0])) for c in ctas])
+    for k in sorted(set(nitems.tolist())):
+        sel = nitems == k
+        print(f"  CTAs with {k} item(s): {sel.sum():3d}, end median {np.median(en[sel]):6.2f} us, "
+              f"busy median {np.median((en - st)[sel]):6.2f} us")
     print("  end by CTA index (0-147 | 148-295) medians:", np.median(en[:148]).round(2), np.median(en[148:]).round(2))
     tk = np.zeros((1024, 8), np.uint64)
     _abi.check(_abi._lib.absp_debug_topk_trace(tk.ctypes.data, tk.nbytes))
