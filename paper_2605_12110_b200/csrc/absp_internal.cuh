@@ -67,6 +67,10 @@ struct LayerView {
     float* scales_min;
     float* zps_min;
     float* scores;      // [seg]
+    // quantization statistics (build_store.cu)
+    float* qstat;       // frozen per-channel statistics [arrays][units][2][d]
+    float* qpart;       // build scratch: per-slice statistics [arrays][units][slices][2][d]
+    uint32_t* wmask;    // decode-time maintenance: changed code words [arrays][units]
 };
 
 // Packed code rows: centroid i of a unit occupies W = D*bits/32 consecutive words

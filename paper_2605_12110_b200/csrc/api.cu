@@ -79,7 +79,10 @@ struct WorkList {
     DevBuf<uint32_t> page;    // resolved page list, [n_work][ns] (see PageList)
     DevBuf<uint16_t> valid;
     uint32_t n_work = 0, max_runs = 0, ns = 0, grid = 0;
+    std::vector<uint32_t> h_base, h_run;  // host copies: an unchanged list is not re-uploaded
     void release() {
+        h_base.clear();
+        h_run.clear();
         chunk_unit.release();
         chunk_idx.release();
         chunk_base.release();
@@ -91,8 +94,64 @@ struct WorkList {
     PageList pages() const { return PageList{page.p, valid.p, chunk_base.p, ns}; }
 };
 
+// Host->device uploads of layout data. Synchronous (cudaMemcpy) when no stream is
+// given; otherwise staged through a pinned buffer and copied with cudaMemcpyAsync on
+// the stream, in order with the kernels around it (decode-time appends).
+struct Stager {
+    cudaStream_t s = nullptr;
+    bool async = false;
+    unsigned char* host = nullptr;  // pinned, owned by the layer
+    size_t cap = 0, off = 0;
+    cudaEvent_t done = nullptr;     // recorded after the last async batch
+    cudaError_t begin(cudaStream_t stream, bool use_async) {
+        s = stream;
+        async = use_async;
+        off = 0;
+        if (async && done) return cudaEventSynchronize(done);  // the previous batch has been read
+        return cudaSuccess;
+    }
+    cudaError_t put(void* dst, const void* src, size_t bytes) {
+        if (bytes == 0) return cudaSuccess;
+        if (!async) return cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+        const size_t need = (off + bytes + 15) & ~size_t(15);
+        if (need > cap) {  // grow: earlier copies of this batch must have left the old buffer
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return e;
+            if (host) cudaFreeHost(host);
+            host = nullptr;
+            cap = std::max<size_t>(2 * need, 1 << 16);
+            e = cudaMallocHost(&host, cap);
+            if (e != cudaSuccess) { host = nullptr; cap = 0; return e; }
+            off = 0;
+        }
+        std::memcpy(host + off, src, bytes);
+        cudaError_t e = cudaMemcpyAsync(dst, host + off, bytes, cudaMemcpyHostToDevice, s);
+        off = (off + bytes + 15) & ~size_t(15);
+        return e;
+    }
+    cudaError_t zero(void* dst, size_t bytes) {
+        return async ? cudaMemsetAsync(dst, 0, bytes, s) : cudaMemset(dst, 0, bytes);
+    }
+    cudaError_t end() {
+        if (!async) return cudaSuccess;
+        if (!done) {
+            cudaError_t e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaEventRecord(done, s);
+    }
+    void release() {
+        if (done) cudaEventDestroy(done);
+        if (host) cudaFreeHost(host);
+        done = nullptr;
+        host = nullptr;
+        cap = off = 0;
+    }
+};
+
 struct Layer {
     bool assigned = false, bound = false, built = false, selected = false;
+    Stager stager;
     std::vector<uint32_t> block_sizes;
     const uint16_t* k_pool = nullptr;
     const uint16_t* v_pool = nullptr;
@@ -119,8 +178,11 @@ struct Layer {
     DevBuf<uint32_t> ready;   // decode step: per-unit "selection published" flags (zero between steps)
     DevBuf<uint32_t> scored;  // per-unit scored-centroid counters (zero between steps)
     DevBuf<uint32_t> topk_units;  // units grouped by top-k register class
+    std::vector<uint32_t> h_topk_order;
     TopkClasses topk_classes{};
     DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
+    DevBuf<float> qstat, qpart;     // frozen quantization statistics, build scratch
+    DevBuf<uint32_t> wmask;         // decode-time maintenance: changed code words
     DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
     DevBuf<uint16_t> stage_q;
     DevBuf<float> stage_out;
@@ -149,6 +211,8 @@ struct Layer {
         sel_blocks.release(); sel_counts.release(); ready.release(); scored.release(); topk_units.release();
         approx.release(); unit_err.release();
         part_o.release(); part_ml.release();
+        qstat.release(); qpart.release(); wmask.release();
+        stager.release();
         stage_q.release(); stage_out.release();
         drop_host_graph();
         step_work.release();
@@ -200,6 +264,9 @@ LayerView view_of(absp_ctx* ctx, Layer& l) {
     v.scales_min = l.scales_min.p;
     v.zps_min = l.zps_min.p;
     v.scores = l.scores.p;
+    v.qstat = l.qstat.p;
+    v.qpart = l.qpart.p;
+    v.wmask = l.wmask.p;
     return v;
 }
 
@@ -222,7 +289,7 @@ uint32_t chunks_for(uint32_t entries, uint32_t block) {
 // decode, blocks_stride for explicit selections), the CTA runs of every unit under
 // the persistent attention grid, and sizes the partial buffers.
 absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t cap, int num_sms,
-                       WorkList& wl) {
+                       WorkList& wl, Stager* up = nullptr) {
     std::vector<uint32_t> base(l.desc.size() + 1, 0), unit_of, idx_of;
     for (size_t u = 0; u < l.desc.size(); ++u) {
         const UnitDesc& d = l.desc[u];
@@ -250,20 +317,25 @@ absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t c
         run[u] = first | ((last - first + 1) << 16);
         wl.max_runs = std::max(wl.max_runs, last - first + 1);
     }
+    if (up && up->async && wl.chunk_base.p && base == wl.h_base && run == wl.h_run) return ABSP_OK;  // unchanged
+    Stager sync_up;
+    Stager& st = up ? *up : sync_up;
     const size_t n_slots = size_t(wl.n_work) * wl.ns;
     ABSP_CUDA(wl.page.ensure(n_slots));
     ABSP_CUDA(wl.valid.ensure(n_slots));
-    ABSP_CUDA(cudaMemset(wl.valid.p, 0, n_slots * 2));
+    ABSP_CUDA(st.zero(wl.valid.p, n_slots * 2));
     ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
     ABSP_CUDA(wl.chunk_idx.ensure(idx_of.size()));
     ABSP_CUDA(wl.chunk_base.ensure(base.size()));
     ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
     ABSP_CUDA(wl.unit_run.ensure(l.desc.size()));
-    ABSP_CUDA(cudaMemcpy(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4, cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4, cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(wl.chunk_base.p, base.data(), base.size() * 4, cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(wl.unit_run.p, run.data(), run.size() * 4, cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemset(wl.unit_done.p, 0, l.desc.size() * 4));
+    ABSP_CUDA(st.put(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4));
+    ABSP_CUDA(st.put(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4));
+    ABSP_CUDA(st.put(wl.chunk_base.p, base.data(), base.size() * 4));
+    ABSP_CUDA(st.put(wl.unit_run.p, run.data(), run.size() * 4));
+    ABSP_CUDA(st.zero(wl.unit_done.p, l.desc.size() * 4));
+    wl.h_base = base;
+    wl.h_run = run;
     // one partial slot per (unit, CTA run, consumer warp)
     ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 8 * D));
     ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 16));
@@ -289,7 +361,7 @@ AttendWork work_view(const WorkList& wl) {
 // and device buffers of a bound layer for its current seq_lens; used by kv_bind and,
 // after every sequence grew by a token, by absp_append (the store stays valid:
 // segments are reserved for max_seq_len, so no growth moves another unit's data).
-static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
+static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = nullptr, bool async = false) {
     const absp_config& c = ctx->cfg;
     const uint32_t batch = l->batch;
     const uint32_t* seq_lens = l->seq_lens.data();
@@ -348,7 +420,7 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
     const bool mm = c.centroid_method == ABSP_CENTROID_MAXMIN;
     const size_t W = words_per_centroid(c);
     ABSP_CUDA(l->d_desc.ensure(units));
-    ABSP_CUDA(l->d_items.ensure(l->items.size()));
+    ABSP_CUDA(l->d_items.ensure(units + l->item_begin.size()));  // bound on items: appends never regrow it
     ABSP_CUDA(l->d_item_begin.ensure(l->item_begin.size()));
     ABSP_CUDA(l->values.ensure(l->total_cap * D));
     if (mm) ABSP_CUDA(l->values_min.ensure(l->total_cap * D));
@@ -361,6 +433,11 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
             ABSP_CUDA(l->scales_min.ensure(units * D));
             ABSP_CUDA(l->zps_min.ensure(units * D));
         }
+        const size_t arrays = mm ? 2 : 1;
+        const size_t slices = std::max<size_t>(1, ceil_div(l->max_cap, 256u));  // kStatRows
+        ABSP_CUDA(l->qstat.ensure(arrays * units * 2 * D));
+        ABSP_CUDA(l->qpart.ensure(arrays * units * slices * 2 * D));
+        ABSP_CUDA(l->wmask.ensure(arrays * units));
     }
     ABSP_CUDA(l->scores.ensure(l->total_cap));
     ABSP_CUDA(l->approx.ensure(l->total_cap));
@@ -369,9 +446,13 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
     ABSP_CUDA(l->sel_counts.ensure(units));
     ABSP_CUDA(l->ready.ensure(units));
-    ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
     ABSP_CUDA(l->scored.ensure(units));
-    ABSP_CUDA(cudaMemset(l->scored.p, 0, units * 4));
+    if (!async) {  // zero between steps; the step kernels keep them so
+        ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
+        ABSP_CUDA(cudaMemset(l->scored.p, 0, units * 4));
+    }
+    Stager& up = l->stager;
+    ABSP_CUDA(up.begin(stream, async));
     // top-k classes: split only when the largest unit needs the big register variants
     l->topk_classes = TopkClasses{};
     if (topk_items(l->max_nblocks) >= 32 || topk_items(l->max_nblocks) == 0) {
@@ -385,18 +466,18 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l) {
         }
         l->topk_classes.begin[kTopkClasses] = uint32_t(order.size());
         ABSP_CUDA(l->topk_units.ensure(units));
-        ABSP_CUDA(cudaMemcpy(l->topk_units.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
+        if (!async || order != l->h_topk_order) ABSP_CUDA(up.put(l->topk_units.p, order.data(), order.size() * 4));
+        l->h_topk_order = order;
         l->topk_classes.units = l->topk_units.p;
     }
     for (auto& kv : l->attend_work) kv.second.release();
     l->attend_work.clear();
-    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work);
+    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work, &up);
     if (st != ABSP_OK) return st;
-    ABSP_CUDA(cudaMemcpy(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc), cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem),
-                         cudaMemcpyHostToDevice));
-    ABSP_CUDA(cudaMemcpy(l->d_item_begin.p, l->item_begin.data(), l->item_begin.size() * 4,
-                         cudaMemcpyHostToDevice));
+    ABSP_CUDA(up.put(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc)));
+    ABSP_CUDA(up.put(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem)));
+    ABSP_CUDA(up.put(l->d_item_begin.p, l->item_begin.data(), l->item_begin.size() * 4));
+    ABSP_CUDA(up.end());
     return ABSP_OK;
 }
 
@@ -606,10 +687,11 @@ absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const 
                                        static_cast<const uint16_t*>(v_new), s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "append kernel");
-    ABSP_CUDA(cudaStreamSynchronize(s));  // the unit layout below is rewritten synchronously
     for (uint32_t b = 0; b < l->batch; ++b) ++l->seq_lens[b];
     l->drop_host_graph();
-    st = layout_layer(ctx, l);
+    // the grown layout is uploaded on the stream, after the append kernel and before
+    // the refresh (no host synchronisation; segments are capacity-reserved, so nothing moves)
+    st = layout_layer(ctx, l, s, true);
     if (st != ABSP_OK) return st;
     n = 0;
     e = launch_refresh_store(view_of(ctx, *l), l->max_cap, s, &n);

@@ -50,11 +50,68 @@ def test_engine_steps_match_reference(cuda, H, d, P, cands, T, n0, steps):
             assert np.array_equal(got.selection[h], want_sel[h]), (step, h)
         ok, err = within_tol(got.output, want)
         assert ok, (step, err)
-        if step % 10 == 0 or step == steps - 1:
+        if True:  # every step: maintenance is incremental, so any drift would show at once
             st = eng.da.download_store(0, 0)
             rs = ref.store()
             assert np.array_equal(st["offsets"], rs["offsets"]), step
             assert np.array_equal(st["values"].view(np.uint32), rs["values"].view(np.uint32)), step
+            assert np.array_equal(st["codes"], rs["codes"]), step
+            assert np.array_equal(st["scales"].view(np.uint32), rs["scales"].view(np.uint32)), step
+            assert np.array_equal(st["zps"].view(np.uint32), rs["zps"].view(np.uint32)), step
+
+
+def _signed_zero_keys(rng, H, n, d, n0):
+    """Channel 0 >= 0 with whole blocks of -0.0 and +0.0 keys (a -0.0 / +0.0 mean centroid ties
+    the channel minimum: std::min keeps the earlier one); channel 1 the other way round."""
+    x = _bf16_values(rng, (H, n, d))
+    x[:, :, 0] = np.abs(x[:, :, 0])
+    x[:, :, 1] = np.abs(x[:, :, 1])
+    x[:, 64:128, 0] = -0.0
+    x[:, 192:256, 0] = 0.0
+    x[:, 64:128, 1] = 0.0
+    x[:, 192:256, 1] = -0.0
+    x[:, n0 + 5:n0 + 40, 0] = -0.0   # decode-time blocks of zeros too
+    x[:, n0 + 5:n0 + 40, 1] = 0.0
+    return x
+
+
+@pytest.mark.parametrize("method,bits,mode,zeros", [
+    (0, 4, 1, True), (0, 4, 0, True), (1, 8, 0, False), (1, 2, 1, True), (0, 8, 1, False), (0, 0, 1, False),
+])
+def test_engine_maintenance_grid(cuda, method, bits, mode, zeros):
+    """Incremental requantization (frozen statistics + changed-word re-encode) against the
+    reference's requantize-everything step, over the QuantSpec grid, both centroid methods
+    and signed-zero ties; the store is compared after every step."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from gpu_util import within_tol
+    from paper_2605_12110_b200 import BlockAssignment, CentroidMethod, DecodeEngine, EngineConfig, QuantMode, QuantSpec
+    H, d, P, cands, T, n0, steps = 4, 64, 4, (4, 8, 16), 128, 300, 48
+    rng = np.random.default_rng(11 + 3 * bits + method + 7 * mode)
+    bs = [cands[h % len(cands)] for h in range(H)]
+    cap = n0 + steps + 3
+    cfg = EngineConfig(num_heads=H, head_dim=d, page_size=P, candidate_block_sizes=cands, token_budget=T,
+                       centroid_method=CentroidMethod(method),
+                       quant=QuantSpec(bits, QuantMode(mode)) if bits else None)
+    eng = DecodeEngine(cfg, BlockAssignment(bs), cap)
+    ref = O.RefEngine(H, d, P, cands, T, bs, cap, method=method, bits=bits, mode=mode)
+    keys = _signed_zero_keys(rng, H, cap, d, n0) if zeros else _bf16_values(rng, (H, cap, d))
+    vals = _bf16_values(rng, (H, cap, d))
+    eng.prefill(keys[:, :n0], vals[:, :n0], n0)
+    ref.prefill(keys[:, :n0], vals[:, :n0], n0)
+    for step in range(steps):
+        k, v = keys[:, n0 + step], vals[:, n0 + step]
+        q = _bf16_values(rng, (H, d))
+        got = eng.step(k, v, q)
+        want, want_sel, fb = ref.step(k, v, q)
+        for h in range(H):
+            assert np.array_equal(got.selection[h], want_sel[h]), (step, h)
+        ok, err = within_tol(got.output, want)
+        assert ok, (step, err)
+        st = eng.da.download_store(0, 0)
+        rs = ref.store()
+        assert np.array_equal(st["values"].view(np.uint32), rs["values"].view(np.uint32)), step
+        if bits:
             assert np.array_equal(st["codes"], rs["codes"]), step
             assert np.array_equal(st["scales"].view(np.uint32), rs["scales"].view(np.uint32)), step
             assert np.array_equal(st["zps"].view(np.uint32), rs["zps"].view(np.uint32)), step

@@ -28,7 +28,7 @@ pt = torch.arange(B * pps, dtype=torch.int32, device="cuda").reshape(B, pps)
 da.bind(0, k, v, pt, [n] * B)
 da.build_store(0)
 q = torch.empty(B, H * G, d, dtype=torch.int16, device="cuda")
-kn = torch.empty(B, H, d, dtype=torch.int16, device="cuda")
+kn = torch.empty(extra, B, H, d, dtype=torch.int16, device="cuda")  # a fresh token every step
 vn = torch.empty_like(kn)
 for t, s in ((q, 2), (kn, 3), (vn, 4)):
     fill_synthetic_bf16(t, SEED, s)
@@ -37,7 +37,7 @@ times, steps = [], []
 for i in range(extra - 1):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    da.append(0, kn, vn)
+    da.append(0, kn[i], vn[i])
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     da.decode_step(0, q, out)

@@ -73,7 +73,11 @@ for rep in range(2):
     if at[:148, 250].max() > 0:
         print(f"  attn selected     {pct(r(at[:148, 250][at[:148, 250] > 0]))}")
     first = np.array([at[c, 64] for c in range(148)])
+    print(f"  attn first issue  {pct(r(at[:148, 1]))}")
     print(f"  attn first data   {pct(r(first))}")
+    print(f"    issue - start   {pct((at[:148, 1].astype(np.int64) - at[:148, 0].astype(np.int64)) / 1e3)}")
+    print(f"    data - issue    {pct((first.astype(np.int64) - at[:148, 1].astype(np.int64)) / 1e3)}")
+    print(f"    2nd - 1st data  {pct((at[:148, 65].astype(np.int64) - first.astype(np.int64)) / 1e3)}")
     last_arr = np.array([max(at[c, 64:128]) for c in range(148)])
     print(f"  attn last data    {pct(r(last_arr))}")
     ends = np.array([max(at[c, 242:250]) for c in range(148)])
