@@ -231,7 +231,7 @@ __device__ __forceinline__ uint32_t encode_code(float v, float sc, float rc, flo
 constexpr uint32_t kEncodeRows = 256;  // centroid rows per k_encode CTA
 
 template <int D, int BITS>
-__global__ void __launch_bounds__(256) k_encode(LayerView L, const uint32_t* __restrict__ wmask) {
+__global__ void __launch_bounds__(256, BITS == 2 ? 2 : (BITS == 4 ? 3 : 4)) k_encode(LayerView L, const uint32_t* __restrict__ wmask) {
     constexpr uint32_t W = D * BITS / 32, CPW = 32 / BITS, RPI = 256 / W, F4 = CPW / 4;
     const uint32_t u = blockIdx.y;
     const UnitDesc du = L.desc[u];
@@ -264,13 +264,41 @@ __global__ void __launch_bounds__(256) k_encode(LayerView L, const uint32_t* __r
         uint32_t* codes = a ? L.codes_min : L.codes;
         auto encode_row = [&](uint32_t i, const float4* f) {
             uint32_t word = 0;
+            bool exact = !asym;
+            if (asym) {
+                // y = (v - zp) * (1/scale) >= 0; floor(y + 1/2 -+ 2^-10) by a round-down add
+                // of 2^23. Equal floors put no rounding boundary within 2^-10 of y + 1/2, and
+                // |y - fl((v - zp) / scale)| <= 3 * 2^-24 * y, so the floor is the reference's
+                // round-half-away code; otherwise the word is redone with the IEEE division.
+                constexpr float kLo = 0.5f - 0.0009765625f, kHi = 0.5f + 0.0009765625f, kMagic = 8388608.0f;
+                uint32_t diff = 0;
 #pragma unroll
-            for (uint32_t k4 = 0; k4 < F4; ++k4) {
-                const float v[4] = {f[k4].x, f[k4].y, f[k4].z, f[k4].w};
+                for (uint32_t k4 = 0; k4 < F4; ++k4) {
+                    const float v[4] = {f[k4].x, f[k4].y, f[k4].z, f[k4].w};
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k) {
-                    const uint32_t c = k4 * 4 + k;
-                    word |= encode_code(v[k], sc[c], rc[c], zp[c], asym, levels, mid) << (c * BITS);
+                    for (uint32_t k = 0; k < 4; ++k) {
+                        const uint32_t c = k4 * 4 + k;
+                        const float y = __fmul_rn(__fsub_rn(v[k], zp[c]), rc[c]);
+                        const uint32_t qa = __float_as_uint(__fadd_rd(__fadd_rn(y, kLo), kMagic));
+                        const uint32_t qb = __float_as_uint(__fadd_rd(__fadd_rn(y, kHi), kMagic));
+                        diff |= qa ^ qb;
+                        diff |= y < 4096.0f ? 0u : 1u;
+                        const uint32_t q = min(qa - 0x4B000000u, uint32_t(levels));
+                        word |= q << (c * BITS);
+                    }
+                }
+                exact = diff != 0u;
+            }
+            if (exact) {
+                word = 0;
+#pragma unroll
+                for (uint32_t k4 = 0; k4 < F4; ++k4) {
+                    const float v[4] = {f[k4].x, f[k4].y, f[k4].z, f[k4].w};
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) {
+                        const uint32_t c = k4 * 4 + k;
+                        word |= encode_code(v[k], sc[c], rc[c], zp[c], asym, levels, mid) << (c * BITS);
+                    }
                 }
             }
             codes[(du.seg + i) * W + code_word_pos(i, w, W)] = word;
