@@ -11,11 +11,11 @@
 //                    tensor cores: w_c = q_c * s_c ~ sigma * (h_c + l_c / 256) with
 //                    int8 h, l, and the u8 codes taken straight from the packed words
 //                    (mma.sync m16n8k32 u8 x s8 -> s32, exact). Per unit
-//                    |A_i - S_i| <= E_u = 2^-10 * sum_c |q_c| (|zp_c| + 15 |s_c|)
+//                    |A_i - S_i| <= E_u = 2^-14 * sum_c |q_c| (|zp_c| + 15 |s_c|)
 //                                        + 15 * sum_c |w_c - sigma (h_c + l_c/256)|:
-//                    the first term has > 100x margin over the serial fp32 sum
-//                    (127u) and the linearisation (3u), the second is the weight
-//                    quantisation exactly (codes <= 15).
+//                    the first term has a 7x margin over the serial fp32 sum
+//                    (~130u) plus the approximation's own roundings (~15u), the
+//                    second is the weight quantisation exactly (codes <= 15).
 //   k_select_refine: one CTA per unit. a = (K-1)-th largest A over blocks
 //                    [0, N-1); every block of the exact top-(K-1) has
 //                    S >= tau >= a - E, hence A >= a - 2E: the candidates
@@ -246,9 +246,14 @@ __global__ void __launch_bounds__(kABlock, kScoreCtasPerSm) k_score_approx(Layer
             bound += rd[16 + i];
             res += rd[24 + i];
         }
-        // |approx - exact| <= 2^-10 sum |q|(|zp| + 15|s|) (fp32 sum, linearisation)
-        //                    + 15 sum |w - sigma (h + l/256)| (weight quantisation)
-        if (tid == 0) err[it.unit] = bound * 0x1p-10f + 15.0f * res * 1.01f;  // same in every CTA of the unit
+        // |approx - exact| <= 2^-14 sum |q|(|zp| + 15|s|) + 15 sum |w - sigma (h + l/256)|.
+        // First term: the exact score's serial fp32 sum of 128 rounded products deviates
+        // from the real-valued sum by <= ~130u sum |q|(|zp| + 15|s|) (u = 2^-24), and the
+        // approximation's own roundings (w = q s, alpha's tree sum, the int -> float
+        // conversions, sigma scaling, + alpha) by <= ~15u of the same sum: 145u ~ 2^-16.8,
+        // so 2^-14 keeps a 7x margin. Second term: the weight quantisation, exactly
+        // (codes <= 15; 1.01 covers the rounding of res itself).
+        if (tid == 0) err[it.unit] = bound * 0x1p-14f + 15.0f * res * 1.01f;  // same in every CTA of the unit
         // B fragments: b0 = logical k 4t4..4t4+3, b1 = 16 + 4t4.., column g (0: h, 1: l)
         uint32_t bfr[KS][2];
 #pragma unroll
@@ -585,19 +590,37 @@ __global__ void __launch_bounds__(kRThreads, 1) k_select_refine(LayerView L, con
         if (Cn <= kRankCap) {
             // position = rank among the candidates (composites are distinct), shifted by
             // one past the trailing block when it ranks higher
-            if (tid == 0) st[5] = 0u;
-            __syncthreads();
-            for (uint32_t jj = tid; jj < Cn; jj += kRThreads) {
-                const unsigned long long me = comp[jj];
-                uint32_t rank = 0;
-                for (uint32_t o = 0; o < Cn; ++o) rank += comp[o] > me;
-                if (rank < K1) {
-                    const bool below = ct > me;
-                    outs[rank + (below ? 1u : 0u)] = ~uint32_t(me);
-                    if (!below && !all) atomicAdd(&st[5], 1u);
+            // Placement by rank: tpc adjacent lanes share an element (each counts a strided
+            // share with four independent partial counts); the cost is m^2 / 32 shared loads.
+            auto place = [&](const unsigned long long* arr, uint32_t m) {
+                if (tid == 0) st[5] = 0u;
+                __syncthreads();
+                const uint32_t tpc = m <= kRThreads / 8 ? 8u : m <= kRThreads / 4 ? 4u : m <= kRThreads / 2 ? 2u : 1u;
+                const uint32_t part = tid % tpc;
+                for (uint32_t jb = 0; jb < m * tpc; jb += kRThreads) {  // uniform trip count
+                    const uint32_t jj = (jb + tid) / tpc;
+                    const bool live = jb + tid < m * tpc;
+                    const unsigned long long me = live ? arr[jj] : ~0ull;
+                    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+                    uint32_t o = part;
+                    for (; o + 3 * tpc < m; o += 4 * tpc) {
+                        r0 += arr[o] > me;
+                        r1 += arr[o + tpc] > me;
+                        r2 += arr[o + 2 * tpc] > me;
+                        r3 += arr[o + 3 * tpc] > me;
+                    }
+                    for (; o < m; o += tpc) r0 += arr[o] > me;
+                    uint32_t rank = r0 + r1 + r2 + r3;
+                    for (uint32_t off = 1; off < tpc; off <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
+                    if (live && part == 0 && rank < K1) {
+                        const bool below = ct > me;
+                        outs[rank + (below ? 1u : 0u)] = ~uint32_t(me);
+                        if (!below && !all) atomicAdd(&st[5], 1u);
+                    }
                 }
-            }
-            __syncthreads();
+                __syncthreads();
+            };
+            place(comp, Cn);
             if (tid == 0 && !all) outs[st[5]] = N - 1;
         } else {
             sort_desc(comp, Cn);

@@ -116,6 +116,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     const int my_items = REG ? ITEMS : int((nsteps + kWarps - 1 - warp) / kWarps);
 
     griddep_launch_dependents();
+    {   // the page resolution at the end reads the sequence's page-table row: the H units of
+        // the sequence warm L2 with a slice each while the scores are being produced
+        const uint32_t row_pages = (du.n_tokens + L.P - 1) / L.P;
+        const uint32_t slice = (row_pages + L.H - 1) / L.H;
+        const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+        for (uint32_t p = du.head * slice + threadIdx.x * 32; p < min(row_pages, (du.head + 1) * slice);
+             p += blockDim.x * 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pt + p));
+    }
     if (scored) {
         // the unit's scores are complete once the scorer's producers have published all
         // N of them (release); then re-arm the counter for the next step

@@ -15,6 +15,9 @@ from paper_2605_12110_b200 import _abi  # noqa: E402
 _abi._lib = _abi.load(ROOT / "paper_2605_12110_b200" / "lib" / "libabsp_trace.so")
 for f in ("absp_debug_score_trace", "absp_debug_topk_trace", "absp_debug_attn_trace"):
     getattr(_abi._lib, f).argtypes = [C.c_void_p, C.c_size_t]
+_abi._lib.absp_debug_refine_trace.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t]
+import os  # noqa: E402
+FAST = os.environ.get("ABSP_FAST_SELECT", "") == "1"
 from bench import SEED, WORKLOADS  # noqa: E402
 from paper_2605_12110_b200 import (BlockAssignment, DecodeAttention, EngineConfig, QuantSpec,  # noqa: E402
                                    fill_synthetic_bf16)
@@ -56,13 +59,27 @@ for rep in range(2):
     _abi.check(_abi._lib.absp_debug_topk_trace(tk.ctypes.data, tk.nbytes))
     _abi.check(_abi._lib.absp_debug_attn_trace(at.ctypes.data, at.nbytes))
     ns = 2 * 148
+    if FAST:  # tensor-core filter + refine: time base = first refine CTA start
+        rf = np.zeros((1024, 8), np.uint64)
+        cand = np.zeros(1024, np.uint32)
+        _abi.check(_abi._lib.absp_debug_refine_trace(rf.ctypes.data, rf.nbytes, cand.ctypes.data, cand.nbytes))
+        units = B * H
+        t0 = int(rf[:units, 0].min())
+        r = lambda a: (a.astype(np.int64) - t0) / 1e3
+        print(f"rep {rep} (us from the first refine CTA start; pctl 0/10/50/90/100)")
+        for j, nm in enumerate(["start", "after griddep wait", "loads", "kth bound", "candidates+table",
+                                "exact scored", "ordered", "end"]):
+            print(f"  refine {nm:18s} {pct(r(rf[:units, j]))}")
+        sc[:] = 0
+        sc[:, 0] = t0
     t0 = int(sc[:ns, 0].min())
     r = lambda a: (a.astype(np.int64) - t0) / 1e3
     units = B * H
-    print(f"rep {rep} (us from the first scorer CTA start; pctl 0/10/50/90/100)")
-    print(f"  scorer start      {pct(r(sc[:ns, 0]))}")
-    print(f"  scorer end        {pct(r(sc[:ns, 1]))}")
-    if tk[:units, 0].max() >= sc[:ns, 0].min():
+    if not FAST:
+        print(f"rep {rep} (us from the first scorer CTA start; pctl 0/10/50/90/100)")
+        print(f"  scorer start      {pct(r(sc[:ns, 0]))}")
+        print(f"  scorer end        {pct(r(sc[:ns, 1]))}")
+    if not FAST and tk[:units, 0].max() >= sc[:ns, 0].min():
         print(f"  topk start        {pct(r(tk[:units, 0]))}")
         for j, nm in ((1, "topk keys issued"), (2, "topk threshold"), (3, "topk compacted"), (4, "topk ordered")):
             v = tk[:units, j]
