@@ -115,6 +115,7 @@ cudaError_t launch_append_rows(const LayerView& L, const uint16_t* k_new, const 
 cudaError_t launch_score(const LayerView& L, const uint16_t* q, const ScoreWork& work, cudaStream_t s,
                          int* launches);
 cudaError_t init_score_attributes();  // per device, once
+cudaError_t init_topk_attributes();   // per device, once
 // Selected blocks resolved to pool pages, laid out by global attention chunk:
 // unit u's slot s = entry * (B/P) + page lives at index chunk_base[u] * ns + s, so
 // chunk w's slots are [w * ns, (w + 1) * ns). Written by the top-k kernel (decode

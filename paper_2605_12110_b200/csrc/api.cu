@@ -558,6 +558,7 @@ absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) 
                                     std::to_string(prop.major) + std::to_string(prop.minor));
     ABSP_CUDA(init_attend_attributes());
     ABSP_CUDA(init_score_attributes());
+    ABSP_CUDA(init_topk_attributes());
     ABSP_CUDA(init_select_attributes());
     auto* ctx = new absp_ctx;
     ctx->device = device;

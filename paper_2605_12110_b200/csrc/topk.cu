@@ -69,14 +69,23 @@ struct TopkSmem {
     } u;
 };
 
-template <bool REG, int ITEMS>
+// Keys of a unit, thread (warp, lane) owning keys i = (j * kWarps + warp) * 32 + lane:
+// in registers (REG), in dynamic shared memory (SMK: the largest units, whose
+// register arrays would spill), or re-read from L2.
+template <bool REG, int ITEMS, bool SMK>
 struct Keys {
-    uint32_t r[REG ? ITEMS : 1];
+    uint32_t r[REG && !SMK ? ITEMS : 1];
+    const uint32_t* sk;  // SMK: [n_cand] in shared memory
     const float* sc;
     uint32_t n_cand;
     __device__ __forceinline__ uint32_t get(int j, uint32_t i) const {
+        if (SMK) return sk[i];
         if (REG) return r[j];
         return i < n_cand ? order_key(__ldg(sc + i)) : 0u;
+    }
+    __device__ __forceinline__ uint32_t reg(int j, uint32_t warp, uint32_t lane) const {
+        if (SMK) return sk[(j * kWarps + warp) * 32 + lane];
+        return r[j];
     }
 };
 
@@ -98,7 +107,7 @@ __device__ __forceinline__ uint32_t bin_count(bool in, uint32_t key, uint32_t pr
     return __popc(mm);
 }
 
-template <bool REG, int ITEMS>
+template <bool REG, int ITEMS, bool SMK>
 __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blocks, uint32_t stride,
                                                    uint32_t* counts, PageList pages, uint32_t* ready,
                                                    uint32_t* scored, const uint32_t* __restrict__ unit_list) {
@@ -137,10 +146,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
         griddep_wait();  // the scores are written by the scoring kernel of this step
     }
     const float tail_score = N > K ? __ldg(sc + N - 1) : 0.0f;  // the trailing block, loaded early
-    Keys<REG, ITEMS> keys;
+    Keys<REG, ITEMS, SMK> keys;
     keys.sc = sc;
     keys.n_cand = n_cand;
-    if (REG) {
+    extern __shared__ uint32_t topk_keys[];  // SMK only: ITEMS * kThreads keys
+    keys.sk = topk_keys;
+    if (SMK) {
+#pragma unroll 16
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t i = (j * kWarps + warp) * 32 + lane;
+            topk_keys[i] = i < n_cand ? order_key(__ldg(sc + i)) : 0u;
+        }
+    } else if (REG) {
 #pragma unroll
         for (int j = 0; j < (REG ? ITEMS : 1); ++j) {
             const uint32_t i = (j * kWarps + warp) * 32 + lane;
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
         for (int gi = 0; gi < NG; ++gi) {
             uint32_t mx = 0;
 #pragma unroll
-            for (int j = gi * GS; j < gi * GS + GS; ++j) mx = max(mx, keys.r[j]);  // invalid keys are 0
+            for (int j = gi * GS; j < gi * GS + GS; ++j) mx = max(mx, keys.reg(j, warp, lane));  // invalid keys are 0
             gmax[gi] = mx;
         }
         uint32_t kand = 0xffffffffu, kor = 0u;
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
         const uint32_t x = prefix;  // bucket lower edge: low bits zero
         uint32_t c = 0;
 #pragma unroll
-        for (int j = 0; j < ITEMS; ++j) c += keys.r[j] >= x && (j * kWarps + warp) * 32 + lane < n_cand;
+        for (int j = 0; j < ITEMS; ++j) c += keys.reg(j, warp, lane) >= x && (j * kWarps + warp) * 32 + lane < n_cand;
         c = __reduce_add_sync(0xffffffffu, c);
         __syncthreads();
         if (lane == 0) sm.red[0][warp] = c;
@@ -258,9 +275,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
 #pragma unroll
             for (int j = 0; j < ITEMS; ++j) {
                 const uint32_t i = (j * kWarps + warp) * 32 + lane;
-                const bool in = i < n_cand && keys.r[j] >= x;
+                const uint32_t kj = keys.reg(j, warp, lane);
+                const bool in = i < n_cand && kj >= x;
                 const uint32_t m = __ballot_sync(0xffffffffu, in);
-                if (in) sm.sel[pos + __popc(m & ((1u << lane) - 1u))] = (uint64_t(keys.r[j]) << 32) | uint32_t(~i);
+                if (in) sm.sel[pos + __popc(m & ((1u << lane) - 1u))] = (uint64_t(kj) << 32) | uint32_t(~i);
                 pos += __popc(m);
             }
             __syncthreads();
@@ -586,12 +604,23 @@ uint32_t topk_items(uint32_t n_blocks) {
     return 0;
 }
 
-template <bool REG, int IT>
+template <bool REG, int IT, bool SMK = false>
 cudaError_t topk_launch(const LayerView& L, uint32_t grid, uint32_t* blocks, uint32_t stride, uint32_t* counts,
                         const PageList& pages, uint32_t* ready, uint32_t* scored, const uint32_t* unit_list,
                         cudaStream_t s) {
-    return launch_pdl(k_topk<REG, IT>, dim3(grid), dim3(kThreads), 0, s, L, blocks, stride, counts, pages, ready,
-                      scored, unit_list);
+    return launch_pdl(k_topk<REG, IT, SMK>, dim3(grid), dim3(kThreads), SMK ? size_t(IT) * kThreads * 4 : 0, s, L,
+                      blocks, stride, counts, pages, ready, scored, unit_list);
+}
+
+cudaError_t init_topk_attributes() {  // the shared-memory key variants: 32 / 64 / 128 KB of keys
+    cudaError_t e = cudaFuncSetAttribute(k_topk<true, 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         16 * kThreads * 4);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_topk<true, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             32 * kThreads * 4);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_topk<true, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                64 * kThreads * 4);
 }
 
 cudaError_t launch_topk_class(const LayerView& L, uint32_t items, uint32_t grid, uint32_t* blocks, uint32_t stride,
@@ -602,9 +631,10 @@ cudaError_t launch_topk_class(const LayerView& L, uint32_t items, uint32_t grid,
         case 2: return topk_launch<true, 2>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
         case 4: return topk_launch<true, 4>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
         case 8: return topk_launch<true, 8>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
-        case 16: return topk_launch<true, 16>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
-        case 32: return topk_launch<true, 32>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
-        case 64: return topk_launch<true, 64>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 16: return topk_launch<true, 16, true>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        case 32: return topk_launch<true, 32, true>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
+        // 64 keys per thread would spill from registers: they live in shared memory
+        case 64: return topk_launch<true, 64, true>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
         default: return topk_launch<false, 1>(L, grid, blocks, stride, counts, pages, ready, scored, unit_list, s);
     }
 }

@@ -111,10 +111,10 @@ int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const size_t read_bytes = size_t(1) << 30;  // bytes moved per run
-    struct Cfg { uint32_t page, stage, stages; };
-    std::vector<Cfg> cfgs = {{4096, 65536, 3}, {4096, 32768, 6}, {4096, 49152, 4}, {4096, 16384, 12},
-                             {2048, 32768, 6}, {1024, 32768, 6}};
-    const long long holds[] = {0, 1000, 2000, 3000, 4000};  // SM cycles (~0.5 ns each)
+    struct Cfg { uint32_t page, stage, stages, run; };  // run: consecutive pages per random start
+    std::vector<Cfg> cfgs = {{4096, 65536, 3, 1}, {2048, 65536, 3, 1}, {1024, 65536, 3, 1},
+                             {1024, 65536, 3, 4}, {1024, 65536, 3, 16}, {2048, 65536, 3, 8}};
+    const long long holds[] = {0, 2000};  // SM cycles (~0.5 ns each)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -123,7 +123,10 @@ int main(int argc, char** argv) {
         const uint32_t pool_pages = uint32_t(pool_bytes / c.page);
         std::vector<uint32_t> perm(n_pages);
         srand(1);
-        for (uint32_t i = 0; i < n_pages; ++i) perm[i] = uint32_t((uint64_t(rand()) * 65536 + rand()) % pool_pages);
+        for (uint32_t i = 0; i < n_pages; i += c.run) {
+            const uint32_t start = uint32_t((uint64_t(rand()) * 65536 + rand()) % (pool_pages - c.run));
+            for (uint32_t j = 0; j < c.run && i + j < n_pages; ++j) perm[i + j] = start + j;
+        }
         uint32_t* dperm;
         cudaMalloc(&dperm, n_pages * 4);
         cudaMemcpy(dperm, perm.data(), n_pages * 4, cudaMemcpyHostToDevice);
@@ -141,8 +144,8 @@ int main(int argc, char** argv) {
                 if (rep) best = ms < best ? ms : best;
             }
             cudaError_t err = cudaGetLastError();
-            printf("bulk page=%5u stage=%6u stages=%2u hold=%5lld cyc : %7.1f GB/s %s\n", c.page, c.stage, c.stages,
-                   hold, read_bytes / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
+            printf("bulk page=%5u run=%2u stage=%6u stages=%2u hold=%5lld cyc : %7.1f GB/s %s\n", c.page, c.run, c.stage,
+                   c.stages, hold, read_bytes / (best * 1e-3) / 1e9, err ? cudaGetErrorString(err) : "");
         }
         cudaFree(dperm);
     }
