@@ -40,7 +40,9 @@ class Layer:
 
 
 def make_layer(seed, H=8, G=4, d=128, P=16, block_sizes=(16, 32, 64), seq_lens=(1000,), extra_pages=3,
-               scale=1.0, kv=None, q=None) -> Layer:
+               scale=1.0, kv=None, q=None, sequential=False, swaps=0) -> Layer:
+    """sequential: pages handed out in order (the reference allocator, kv_cache.cpp:53-60),
+    with `swaps` random page pairs exchanged to break some contiguous runs."""
     rng = np.random.default_rng(seed)
     bs = [block_sizes[h % len(block_sizes)] for h in range(H)] if len(block_sizes) != H else list(block_sizes)
     pages_per = [(n + P - 1) // P for n in seq_lens]
@@ -51,6 +53,11 @@ def make_layer(seed, H=8, G=4, d=128, P=16, block_sizes=(16, 32, 64), seq_lens=(
     else:
         kf, vf = kv
     perm = rng.permutation(pool_pages).astype(np.uint32)
+    if sequential:
+        perm = np.arange(pool_pages, dtype=np.uint32)
+        for _ in range(swaps):
+            a, b = rng.integers(0, pool_pages, 2)
+            perm[a], perm[b] = perm[b], perm[a]
     max_pages = max(pages_per) + 1
     pt = np.zeros((len(seq_lens), max_pages), np.uint32)
     o = 0

@@ -100,6 +100,32 @@ def test_random_batches_vs_oracle(cuda, G, H, P, cands, seq_lens, T):
         assert ok, f"seq {b}: max abs err {err}"
 
 
+@pytest.mark.parametrize("P,cands,swaps", [
+    (4, (4, 8, 16, 32, 64), 0),    # cfg 5 shape: B >= 16 chunks load as 16-row runs
+    (4, (16, 32, 64), 25),          # some runs broken by swapped pages: per-page fallback
+    (8, (8, 16, 32), 0),            # cfg 1 shape
+    (2, (16, 32), 9),
+    (1, (16, 64), 0),
+])
+def test_sequential_pages_run_copies(cuda, P, cands, swaps):
+    """Sequentially allocated pages (the reference's allocator) with P < 16: attention chunks
+    made of whole 16-row runs of consecutive pages are copied run-wise (attend.cu); the
+    output must not change."""
+    from gpu_util import GpuLayer, within_tol
+    seq_lens, T = (7001, 4096), 1024
+    layer = make_layer(P * 31 + swaps, H=8, G=8, d=128, P=P, block_sizes=cands, seq_lens=seq_lens,
+                       sequential=True, swaps=swaps)
+    gl = GpuLayer(layer, T, 0, 4, 1, max_seq_len=max(seq_lens) + 100)
+    sel = gl.select()
+    out = gl.decode()
+    for b in range(layer.batch):
+        seq, sc, want_sel, want = oracle_step(layer, b, T)
+        for h in range(layer.H):
+            assert np.array_equal(sel[b][h], want_sel[h]), (b, h)
+        ok, err = within_tol(out[b], want)
+        assert ok, f"seq {b}: max abs err {err}"
+
+
 @pytest.mark.parametrize("method,bits,mode", [(0, 4, 0), (0, 8, 1), (0, 2, 0), (0, 0, 1), (1, 4, 1), (1, 8, 0), (1, 0, 1)])
 def test_quant_grid_vs_oracle(cuda, method, bits, mode):
     from gpu_util import GpuLayer
