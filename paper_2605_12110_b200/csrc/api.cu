@@ -393,26 +393,50 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
             l->desc.push_back(d);
         }
     }
-    // Scoring split: CTA c gets the flattened centroid range [c*T/grid, (c+1)*T/grid),
-    // cut into per-unit items, so every CTA scores the same number of centroids
-    // whatever the block sizes (no partial last wave).
+    // Scoring split: contiguous ranges of the flattened centroids, cut into per-unit
+    // items, balanced on rows + kItemCost per item (a CTA's item switch — table build and
+    // pipeline bubble — costs about as much as ~256 rows, measured: tools/score_trace.py),
+    // so CTAs end together whatever the block sizes (no partial last wave).
     {
+        constexpr double kItemCost = 256.0;
         const uint32_t grid = uint32_t(std::max<uint64_t>(
             1, std::min<uint64_t>(uint64_t(ctx->num_sms) * kScoreCtasPerSm, l->total_centroids)));
-        l->item_begin.assign(grid + 1, 0);
-        uint32_t u = 0;
-        uint64_t ubase = 0;  // flattened index of unit u's first centroid
-        for (uint32_t c = 0; c < grid; ++c) {
-            const uint64_t lo = l->total_centroids * c / grid, hi = l->total_centroids * (c + 1) / grid;
-            l->item_begin[c] = uint32_t(l->items.size());
-            uint64_t pos = lo;
-            while (pos < hi) {
-                while (ubase + l->desc[u].n_blocks <= pos) ubase += l->desc[u++].n_blocks;
-                const uint64_t e = std::min<uint64_t>(hi, ubase + l->desc[u].n_blocks);
-                l->items.push_back({u, uint32_t(pos - ubase), uint32_t(e - ubase), 0u});
-                pos = e;
+        // CTAs the greedy cut needs at a per-CTA cost cap (writes the cut when `out`)
+        auto cut = [&](double cap, bool out) -> uint64_t {
+            uint64_t ctas = 0, pos = 0, ubase = 0;
+            uint32_t u = 0;
+            const uint64_t T = l->total_centroids;
+            while (pos < T) {
+                if (out) l->item_begin[ctas] = uint32_t(l->items.size());
+                const bool last = out && ctas + 1 == grid;
+                double cost = 0.0;
+                bool any = false;
+                while (pos < T) {
+                    while (ubase + l->desc[u].n_blocks <= pos) ubase += l->desc[u++].n_blocks;
+                    const double room = cap - cost - kItemCost;
+                    if (!last && any && room < 1.0) break;
+                    const uint64_t rem = ubase + l->desc[u].n_blocks - pos;
+                    const uint64_t take = last ? rem : std::min<uint64_t>(rem, uint64_t(std::max(1.0, room)));
+                    if (out) l->items.push_back({u, uint32_t(pos - ubase), uint32_t(pos - ubase + take), 0u});
+                    pos += take;
+                    cost += kItemCost + double(take);
+                    any = true;
+                    if (!last && cost >= cap) break;
+                }
+                ++ctas;
             }
+            return ctas;
+        };
+        double lo = double(l->total_centroids) / grid, hi = double(l->total_centroids) / grid + 4 * kItemCost + 2;
+        while (cut(hi, false) > grid) hi *= 1.5;
+        for (int it = 0; it < 40; ++it) {  // smallest cap that fits the grid
+            const double mid = 0.5 * (lo + hi);
+            if (cut(mid, false) <= grid) hi = mid;
+            else lo = mid;
         }
+        l->item_begin.assign(grid + 1, 0);
+        const uint64_t used = cut(hi, true);
+        for (uint64_t c = used; c < grid; ++c) l->item_begin[c] = uint32_t(l->items.size());  // idle CTAs
         l->item_begin[grid] = uint32_t(l->items.size());
     }
     const size_t units = l->desc.size();

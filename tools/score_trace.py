@@ -65,26 +65,6 @@ for rep in range(3):
         print(f"  CTAs with {k} item(s): {sel.sum():3d}, end median {np.median(en[sel]):6.2f} us, "
               f"busy median {np.median((en - st)[sel]):6.2f} us")
     print("  end by CTA index (0-147 | 148-295) medians:", np.median(en[:148]).round(2), np.median(en[148:]).round(2))
-    # per-item segments against the host replica of layout_layer's flat split
-    nb = [-(-n // w["cands"][h % len(w["cands"])]) for _ in range(B) for h in range(H)]
-    tot, grid = sum(nb), len(ctas)
-    ubase = np.concatenate([[0], np.cumsum(nb)])
-    rate = []
-    seg_rows, seg_time = {}, {}
-    for j, c in enumerate(ctas):
-        lo, hi = tot * c // grid, tot * (c + 1) // grid
-        cuts = sorted(set([lo, hi] + [int(x) for x in ubase if lo < x < hi]))
-        rows = np.diff(cuts)
-        marks = [int(tr[c, 2 + i]) for i in range(len(rows))] + [int(tr[c, 1])]
-        durs = np.diff(marks) / 1e3
-        for i, (r_, d_) in enumerate(zip(rows, durs)):
-            key = (len(rows), i)
-            seg_rows.setdefault(key, []).append(r_)
-            seg_time.setdefault(key, []).append(d_)
-    for key in sorted(seg_rows):
-        r_, d_ = np.array(seg_rows[key]), np.array(seg_time[key])
-        print(f"  items={key[0]} seg {key[1]}: rows median {np.median(r_):7.0f}  time median {np.median(d_):6.2f} us"
-              f"  ns/row {1e3 * np.median(d_ / np.maximum(r_, 1)):6.2f}")
     tk = np.zeros((1024, 8), np.uint64)
     _abi.check(_abi._lib.absp_debug_topk_trace(tk.ctypes.data, tk.nbytes))
     units = [u for u in range(B * H) if tk[u, 0] and tk[u, 5]]
