@@ -168,6 +168,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t w_begin = range_begin(blockIdx.x, n_work, gridDim.x);
     const uint32_t w_end = range_begin(blockIdx.x + 1, n_work, gridDim.x);
+    // the producer's first 32 chunk descriptors (layout data, written before any step):
+    // loaded before anything else so no fetch waits on them
+    uint32_t cu_pre = 0, ci_pre = 0;
+    if (warp == kWarps && w_begin + lane < w_end) {
+        cu_pre = __ldg(chunk_unit + w_begin + lane);
+        ci_pre = __ldg(chunk_idx + w_begin + lane);
+    }
 
     if (tid == 0) {
         sh.npend = 0u;
@@ -198,8 +205,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         uint32_t pu = 0xffffffffu;  // last unit whose ready flag was acquired
         auto fetch = [&](uint32_t w, Pref& f) {
             if (w >= w_end) return;
-            f.u = __ldg(chunk_unit + w);
-            f.c = __ldg(chunk_idx + w);
+            if (w - w_begin < 32u) {
+                f.u = __shfl_sync(0xffffffffu, cu_pre, w - w_begin);
+                f.c = __shfl_sync(0xffffffffu, ci_pre, w - w_begin);
+            } else {
+                f.u = __ldg(chunk_unit + w);
+                f.c = __ldg(chunk_idx + w);
+            }
             if (ready && f.u != pu) {  // decode step: the unit's page list must be published
                 pu = f.u;
                 while (ld_acquire(ready + pu) == 0u) __nanosleep(32);

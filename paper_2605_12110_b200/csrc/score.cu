@@ -215,6 +215,11 @@ __global__ void __launch_bounds__(kTblThreads, kScoreCtasPerSm) k_score_tbl(Laye
                 if (chunk >= uint32_t(NS)) {
                     mbar_wait(smem_u32(&bars[NS + st]), ((chunk / NS) - 1) & 1);
                     if (work.scored) publish(st);
+                } else if (chunk == 2) {
+                    // ramp-up: the rest of the ring is requested once the first chunk has
+                    // landed — the kernel-start burst of every CTA's first two chunks then
+                    // clears sooner (the scorer is LDS-bound; two stages ahead suffice)
+                    mbar_wait(smem_u32(&bars[0]), 0);
                 }
                 const uint32_t n = min(uint32_t(kChunkRows), it.end - pos);
                 const uint32_t bar = smem_u32(&bars[st]);
