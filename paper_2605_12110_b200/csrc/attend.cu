@@ -328,7 +328,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
         for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
         float lpart = 0.0f, M = -INFINITY;
-        for (uint32_t base = 0; base < nslots; base += 32) {
+        if (nslots <= 16u) {
+            // the common case (<= 2 CTA runs): every load issued before any is used,
+            // one L2 round trip for the whole merge
+            float v[16][PER];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float* src = pou + size_t(j) * 8 * D;
+                if (uint32_t(j) < nslots) {
+                    if (PER == 4) {
+                        const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+                        v[j][0] = t.x; v[j][1] = t.y; v[j][2 % PER] = t.z; v[j][3 % PER] = t.w;
+                    } else {
+                        const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
+                        v[j][0] = t.x; v[j][1 % PER] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) v[j][i] = 0.0f;
+                }
+            }
+            const float mv = lane < nslots ? __ldcg(mlu + lane * 16) : -INFINITY;
+            const float lv = lane < nslots ? __ldcg(mlu + lane * 16 + 1) : 0.0f;
+            float Mw = mv;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, off));
+            M = Mw;
+            const float wl = (mv == -INFINITY || M == -INFINITY) ? 0.0f : exp2f(mv - M);
+            lpart = wl * lv;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float wj = __shfl_sync(0xffffffffu, wl, j);
+#pragma unroll
+                for (int i = 0; i < PER; ++i) acc[i] += wj * v[j][i];
+            }
+        }
+        for (uint32_t base = 0; base < nslots && nslots > 16u; base += 32) {
             const uint32_t n = min(32u, nslots - base);
             const float mv = lane < n ? __ldcg(mlu + (base + lane) * 16) : -INFINITY;
             const float lv = lane < n ? __ldcg(mlu + (base + lane) * 16 + 1) : 0.0f;
