@@ -86,6 +86,9 @@ for rep in range(2):
             if (v > 0).any():
                 print(f"  {nm:17s} {pct(r(v[v > 0]))}")
         print(f"  topk end (pages)  {pct(r(tk[:units, 5][tk[:units, 5] > 0]))}")
+        te = r(tk[:units, 5])
+        q4 = units // 4
+        print("  topk end by unit quarter (medians):", [round(float(np.median(te[i * q4:(i + 1) * q4])), 2) for i in range(4)])
     print(f"  attn CTA start    {pct(r(at[:148, 0]))}")
     if at[:148, 250].max() > 0:
         print(f"  attn selected     {pct(r(at[:148, 250][at[:148, 250] > 0]))}")
