@@ -193,6 +193,7 @@ struct Layer {
     cudaGraphNode_t h2d_node = nullptr, d2h_node = nullptr;
     const void* host_q = nullptr;
     float* host_out = nullptr;
+    bool out_direct = false;  // the graph's attention writes host_out itself (mapped pinned memory)
     int host_launches = 0;
     void drop_host_graph() {
         if (host_exec) cudaGraphExecDestroy(host_exec);
@@ -201,6 +202,8 @@ struct Layer {
         host_graph = nullptr;
         host_q = nullptr;
         host_out = nullptr;
+        out_direct = false;
+        h2d_node = d2h_node = nullptr;
     }
 
     void release() {
@@ -848,12 +851,19 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
     ABSP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     cudaGraph_t graph = nullptr;
     const uint64_t before = ctx->launches;
+    // Pinned host output the device can address (UVA, same pointer): the attention's LSE
+    // merges write it directly, unit by unit as they complete, instead of a copy after
+    // the kernel. Otherwise (pageable, or not device-addressable) a D2H copy node.
+    cudaPointerAttributes pa{};
+    const bool direct = cudaPointerGetAttributes(&pa, out_host) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost && pa.devicePointer == out_host;
+    cudaGetLastError();
     cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     absp_status st = ABSP_OK;
     if (e == cudaSuccess) {
         e = cudaMemcpyAsync(l->stage_q.p, q_host, nq * sizeof(uint16_t), cudaMemcpyHostToDevice, cap);
-        if (e == cudaSuccess) st = absp_decode_step(ctx, layer, l->stage_q.p, l->stage_out.p, cap);
-        if (e == cudaSuccess && st == ABSP_OK)
+        if (e == cudaSuccess) st = absp_decode_step(ctx, layer, l->stage_q.p, direct ? out_host : l->stage_out.p, cap);
+        if (e == cudaSuccess && st == ABSP_OK && !direct)
             e = cudaMemcpyAsync(out_host, l->stage_out.p, nq * sizeof(float), cudaMemcpyDeviceToHost, cap);
         const cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
         if (e == cudaSuccess) e = e2;
@@ -874,7 +884,7 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
             if (p.kind == cudaMemcpyHostToDevice) l->h2d_node = nodes[i];
             else if (p.kind == cudaMemcpyDeviceToHost) l->d2h_node = nodes[i];
         }
-        if (e == cudaSuccess && (!l->h2d_node || !l->d2h_node)) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess && (!l->h2d_node || (!direct && !l->d2h_node))) e = cudaErrorInvalidValue;
         if (e == cudaSuccess) e = cudaGraphInstantiate(&l->host_exec, graph, 0);
     }
     cudaStreamDestroy(cap);
@@ -891,6 +901,7 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
     }
     l->host_q = q_host;
     l->host_out = out_host;
+    l->out_direct = direct;
     return ABSP_OK;
 }
 
@@ -909,13 +920,17 @@ absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_h
     const cudaStream_t s = cudaStream_t(stream);
     if (!l->host_exec && capture_host_step(ctx, layer, l, q_host, out_host, nq) != ABSP_OK)
         l->drop_host_graph();
+    if (l->host_exec && l->out_direct && out_host != l->host_out) {  // the output is a kernel argument
+        l->drop_host_graph();
+        if (capture_host_step(ctx, layer, l, q_host, out_host, nq) != ABSP_OK) l->drop_host_graph();
+    }
     bool graph_ok = l->host_exec != nullptr;
     if (graph_ok && (q_host != l->host_q || out_host != l->host_out)) {
         // re-point the copy nodes; buffers the graph cannot take (e.g. pageable memory
         // after pinned) run this call eagerly and keep the graph as it is
         cudaError_t e = cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, q_host,
                                                            nq * sizeof(uint16_t), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess)
+        if (e == cudaSuccess && !l->out_direct)
             e = cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, out_host, l->stage_out.p,
                                                    nq * sizeof(float), cudaMemcpyDeviceToHost);
         if (e == cudaSuccess) {
@@ -926,8 +941,9 @@ absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_h
             // the nodes may be half re-pointed: restore them for the next call
             if (cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, l->host_q,
                                                    nq * sizeof(uint16_t), cudaMemcpyHostToDevice) != cudaSuccess ||
-                cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, l->host_out, l->stage_out.p,
-                                                   nq * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+                (!l->out_direct &&
+                 cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, l->host_out, l->stage_out.p,
+                                                    nq * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)) {
                 cudaGetLastError();
                 l->drop_host_graph();
             }

@@ -296,6 +296,10 @@ def test_decode_step_host_matches_device(cuda):
     out3 = torch.zeros(dev.shape, dtype=torch.float32)
     gl.da.decode_step_host(0, torch.from_numpy(layer.q.view(np.int16).copy()), out3)
     assert np.array_equal(out3.numpy(), dev)
+    # back to pinned buffers (the attention writes pinned output directly)
+    out_host.zero_()
+    gl.da.decode_step_host(0, q_host, out_host)
+    assert np.array_equal(out_host.numpy(), dev)
 
 
 def test_synthetic_generator_matches_host_twin(cuda):
