@@ -303,6 +303,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
                 }
                 const uint32_t n_above = __syncthreads_count(above);
                 if (threadIdx.x == 0) sm.nsel = n_above;
+            } else if (C <= 2u * kThreads) {
+                // bitonic sort (descending) of 2 * kThreads composites, zero-padded: warp w
+                // holds elements 64w + lane and 64w + 32 + lane in registers; distances
+                // <= 32 are exchanged by shuffles / within the thread, larger ones through
+                // shared memory (10 of the 55 stages), so most stages need no barrier
+                for (uint32_t i = C + threadIdx.x; i < 2u * kThreads; i += kThreads) sm.sel[i] = 0ull;
+                __syncthreads();
+                const uint32_t p0 = warp * 64 + lane, p1 = p0 + 32;
+                unsigned long long v0 = sm.sel[p0], v1 = sm.sel[p1];
+                auto mx = [](unsigned long long a, unsigned long long b) { return a > b ? a : b; };
+                auto mn = [](unsigned long long a, unsigned long long b) { return a > b ? b : a; };
+                for (uint32_t k = 2; k <= 2u * kThreads; k <<= 1) {
+                    uint32_t j = k >> 1;
+                    if (j >= 64) {  // cross-warp stages through shared memory
+                        sm.sel[p0] = v0;
+                        sm.sel[p1] = v1;
+                        __syncthreads();
+                        for (; j >= 64; j >>= 1) {
+                            for (uint32_t i = threadIdx.x; i < 2u * kThreads; i += kThreads) {
+                                const uint32_t ixj = i ^ j;
+                                if (ixj > i) {
+                                    const unsigned long long a = sm.sel[i], b = sm.sel[ixj];
+                                    if (((i & k) == 0) ? (a < b) : (a > b)) {
+                                        sm.sel[i] = b;
+                                        sm.sel[ixj] = a;
+                                    }
+                                }
+                            }
+                            __syncthreads();
+                        }
+                        v0 = sm.sel[p0];
+                        v1 = sm.sel[p1];
+                    }
+                    if (j == 32) {  // the thread's own pair
+                        const bool desc = (p0 & k) == 0;
+                        const unsigned long long hi = mx(v0, v1), lo = mn(v0, v1);
+                        v0 = desc ? hi : lo;
+                        v1 = desc ? lo : hi;
+                        j = 16;
+                    }
+                    for (; j > 0; j >>= 1) {  // partner lane ^ j, same register
+                        const unsigned long long o0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                        const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                        const bool lower = (lane & j) == 0;
+                        v0 = (lower == ((p0 & k) == 0)) ? mx(v0, o0) : mn(v0, o0);
+                        v1 = (lower == ((p1 & k) == 0)) ? mx(v1, o1) : mn(v1, o1);
+                    }
+                }
+                sm.sel[p0] = v0;
+                sm.sel[p1] = v1;
+                __syncthreads();
+                for (uint32_t p = threadIdx.x; p < K1; p += kThreads) {
+                    const unsigned long long me = sm.sel[p];
+                    out[p + (ct > me ? 1u : 0u)] = ~uint32_t(me);
+                    if (me > ct) atomicAdd(&sm.nsel, 1u);
+                }
             } else {
                 uint32_t sp = 1;
                 while (sp < C) sp <<= 1;
