@@ -75,7 +75,9 @@ __device__ __forceinline__ void resolve_pages(const LayerView& L, const UnitDesc
 
 // Publishes unit u's ordered selection `outs` (shared memory): blocks / counts, the
 // page list for the attention producer and, in the decode step, the unit's ready
-// flag (CTA barrier, then one gpu-scope fence + release store by thread 0).
+// flag (CTA barrier, then a gpu-scope release store by thread 0: release is
+// cumulative over the CTA's writes ordered before it by the barrier, so no separate
+// fence is needed — the same pattern as CUTLASS's semaphore release).
 __device__ __forceinline__ void publish_selection(const LayerView& L, const UnitDesc& du, uint32_t u,
                                                   const uint32_t* outs, uint32_t n, uint32_t* blocks, uint32_t stride,
                                                   uint32_t* counts, const PageList& pages, uint32_t* ready) {
@@ -85,10 +87,8 @@ __device__ __forceinline__ void publish_selection(const LayerView& L, const Unit
     resolve_pages(L, du, u, n, outs, pages);
     if (!ready) return;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
+    if (threadIdx.x == 0)
         asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(ready + u), "r"(1u) : "memory");
-    }
 }
 
 }  // namespace absp

@@ -182,8 +182,12 @@ __global__ void __launch_bounds__(kTblThreads, kScoreCtasPerSm) k_score_tbl(Laye
 #pragma unroll
             for (int i = 0; i < NS; ++i)
                 if (uint32_t(i) == st && pub_len[i]) {
-                    __threadfence();
-                    atomicAdd(work.scored + pub_unit[i], pub_len[i]);
+                    // the consumers' score stores happen-before this (their mbarrier
+                    // arrive releases, the producer's wait acquires, CTA scope); the
+                    // gpu-scope release reduction publishes them cumulatively
+                    asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(work.scored + pub_unit[i]),
+                                 "r"(pub_len[i])
+                                 : "memory");
                     pub_len[i] = 0u;
                 }
         };
