@@ -152,9 +152,12 @@ absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream);
  * page_table[b][n / P] (PagedKVCache::append, kv_cache.cpp:44-70; the caller's
  * page table must map position n) — then refresh_tail_centroids and
  * requantize_heads over every head (centroids.cpp:122-163, quantizer.cpp:113-150),
- * leaving the store equal to one built from scratch on the grown cache. ECAPACITY
- * when a sequence would exceed max_seq_len or its page table. Synchronises the
- * stream (the host-side unit layout grows with the sequences). */
+ * leaving the store equal to one built from scratch on the grown cache (done
+ * incrementally: only code words whose channel parameters changed are re-encoded).
+ * ECAPACITY when a sequence would exceed max_seq_len or its page table. Stream-
+ * ordered, no host synchronisation: the grown unit layout is uploaded on `stream`
+ * (staged through pinned memory), so a layer's appends and decode steps belong on
+ * one stream. */
 absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const void* v_new, void* stream);
 
 /* estimate_scores on the group-summed query + select_topk for every
