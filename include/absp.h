@@ -155,9 +155,11 @@ absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream);
  * leaving the store equal to one built from scratch on the grown cache (done
  * incrementally: only code words whose channel parameters changed are re-encoded).
  * ECAPACITY when a sequence would exceed max_seq_len or its page table. Stream-
- * ordered, no host synchronisation: the grown unit layout is uploaded on `stream`
- * (staged through pinned memory), so a layer's appends and decode steps belong on
- * one stream. */
+ * ordered: the grown unit layout is uploaded on `stream` (staged through a ring of
+ * pinned buffers sized at bind), so a layer's appends and decode steps belong on
+ * one stream; the host waits only if more than 4 appends of the layer are still
+ * queued ahead of the GPU. No device buffer is reallocated (capacity-reserved at
+ * bind); see absp_layout_version for captured graphs. */
 absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const void* v_new, void* stream);
 
 /* estimate_scores on the group-summed query + select_topk for every
@@ -169,6 +171,23 @@ absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* 
  * list of valid, distinct ids per (b,h), count >= 1). out: fp32 device. */
 absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint32_t* blocks,
                         uint32_t blocks_stride, const uint32_t* counts, float* out, void* stream);
+
+/* Validation of the explicit selections given to absp_attend since the last call
+ * (the reference's check_selection / block_to_pages, engine.cpp:212-232,
+ * kv_cache.cpp:118-138): ABSP_EINVAL for an empty selection or a count above
+ * blocks_stride, ABSP_ERANGE for a block id >= N_h or a page-table entry outside the
+ * pools. absp_attend itself never reads out of bounds (offending entries are
+ * dropped, an empty unit's output is zero); this call synchronises `stream` and
+ * clears the flags. */
+absp_status absp_attend_validate(absp_ctx* ctx, uint32_t layer, void* stream);
+
+/* Version of the layer's decode-step layout: bumped by absp_kv_bind and by any
+ * absp_append that changes a kernel argument of absp_decode_step (grid sizes, work
+ * counts — while sequences are shorter than the token budget, or a unit crosses a
+ * top-k size class). Device buffers are capacity-reserved at bind, so a CUDA graph
+ * the caller captured over absp_decode_step / absp_attend_selected stays valid as
+ * long as this value is unchanged. */
+uint64_t absp_layout_version(absp_ctx* ctx, uint32_t layer);
 
 /* sparse_attention over the layer's most recent selection (made by absp_select or
  * absp_decode_step): the attention half of a decode step, e.g. to run it on another

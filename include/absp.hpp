@@ -282,10 +282,14 @@ class DecodeAttention {
                 void* stream = nullptr) {
         check(absp_select(ctx_, layer, q, blocks, stride, counts, stream));
     }
+    // validate = true: the reference's check_selection semantics (synchronises the
+    // stream; std::invalid_argument / std::out_of_range on a bad selection).
     void attend(uint32_t layer, const void* q, const uint32_t* blocks, uint32_t stride,
-                const uint32_t* counts, float* out, void* stream = nullptr) {
+                const uint32_t* counts, float* out, void* stream = nullptr, bool validate = true) {
         check(absp_attend(ctx_, layer, q, blocks, stride, counts, out, stream));
+        if (validate) check(absp_attend_validate(ctx_, layer, stream));
     }
+    uint64_t layout_version(uint32_t layer) const { return absp_layout_version(ctx_, layer); }
     void decode_step(uint32_t layer, const void* q, float* out, void* stream = nullptr) {
         check(absp_decode_step(ctx_, layer, q, out, stream));
     }

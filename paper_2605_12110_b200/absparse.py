@@ -280,10 +280,19 @@ class DecodeAttention:
         check(self._lib.absp_select(self._ctx, layer, _ptr(q), _ptr(blocks), stride, _ptr(counts),
                                     _stream(stream)))
 
-    def attend(self, layer: int, q, blocks, counts, out, stream=None) -> None:
+    def attend(self, layer: int, q, blocks, counts, out, stream=None, validate: bool = True) -> None:
+        """sparse_attention over an explicit selection. validate=True (the reference's
+        semantics) synchronises and raises InvalidArgument / OutOfRange for an empty
+        selection, a count above the stride, a block id or a page id out of range."""
         stride = int(blocks.shape[-1])
         check(self._lib.absp_attend(self._ctx, layer, _ptr(q), _ptr(blocks), stride, _ptr(counts),
                                     _ptr(out), _stream(stream)))
+        if validate:
+            check(self._lib.absp_attend_validate(self._ctx, layer, _stream(stream)))
+
+    def layout_version(self, layer: int) -> int:
+        """Changes when an append alters a kernel argument of decode_step (absp_layout_version)."""
+        return int(self._lib.absp_layout_version(self._ctx, layer))
 
     def attend_selected(self, layer: int, q, out, stream=None) -> None:
         """Attention over the layer's most recent selection (second half of decode_step)."""

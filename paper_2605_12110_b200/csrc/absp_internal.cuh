@@ -145,8 +145,13 @@ cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_b
                         uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
                         uint32_t* ready, uint32_t* scored, const TopkClasses& classes, cudaStream_t s,
                         int* launches);
+// Explicit-selection validation bits (k_resolve_pages -> absp_attend_validate).
+constexpr uint32_t kAttendErrEmpty = 1u;  // a unit with count 0        (invalid_argument)
+constexpr uint32_t kAttendErrBlock = 2u;  // block id >= n_blocks        (out_of_range)
+constexpr uint32_t kAttendErrCount = 4u;  // count > blocks_stride       (invalid_argument)
+constexpr uint32_t kAttendErrPage = 8u;   // page-table entry >= pool_pages (out_of_range)
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
-                                 const uint32_t* counts, const PageList& pages, cudaStream_t s,
+                                 const uint32_t* counts, const PageList& pages, uint32_t* err, cudaStream_t s,
                                  int* launches);
 // Attention work list: all 128-row chunks of all units, unit-major.
 struct AttendWork {

@@ -73,12 +73,16 @@ struct DevBuf {
     }
 };
 
-// Device-side attention work list (see AttendWork).
+// Device-side attention work list (see AttendWork), with its own split-KV partials:
+// the decode-step list and every explicit-selection list (absp_attend) are separate,
+// so building one never frees buffers another (or a captured graph) still uses.
 struct WorkList {
     DevBuf<uint32_t> chunk_unit, chunk_idx, chunk_base, unit_done, unit_run;
     DevBuf<uint32_t> page;    // resolved page list, [n_work][ns] (see PageList)
     DevBuf<uint16_t> valid;
+    DevBuf<float> part_o, part_ml;  // one partial slot per (unit, CTA run, consumer warp)
     uint32_t n_work = 0, max_runs = 0, ns = 0, grid = 0;
+    uint64_t layout = ~0ull;              // layout version the list was built for
     std::vector<uint32_t> h_base, h_run;  // host copies: an unchanged list is not re-uploaded
     void release() {
         h_base.clear();
@@ -90,42 +94,73 @@ struct WorkList {
         unit_run.release();
         page.release();
         valid.release();
+        part_o.release();
+        part_ml.release();
+        layout = ~0ull;
     }
     PageList pages() const { return PageList{page.p, valid.p, chunk_base.p, ns}; }
 };
 
 // Host->device uploads of layout data. Synchronous (cudaMemcpy) when no stream is
-// given; otherwise staged through a pinned buffer and copied with cudaMemcpyAsync on
-// the stream, in order with the kernels around it (decode-time appends).
+// given; otherwise staged through pinned buffers and copied with cudaMemcpyAsync on
+// the stream, in order with the kernels around it (decode-time appends). The pinned
+// buffers form a ring sized at bind time for the largest batch a layout can upload,
+// so an async batch neither grows a buffer nor waits on the GPU unless more than
+// kRing batches of the layer are still queued ahead of it.
 struct Stager {
+    static constexpr int kRing = 4;
+    struct Buf {
+        unsigned char* host = nullptr;  // pinned
+        size_t cap = 0;
+        cudaEvent_t done = nullptr;     // recorded after the batch that used it
+    };
+    Buf ring[kRing];
+    int cur = 0;
     cudaStream_t s = nullptr;
     bool async = false;
-    unsigned char* host = nullptr;  // pinned, owned by the layer
-    size_t cap = 0, off = 0;
-    cudaEvent_t done = nullptr;     // recorded after the last async batch
+    size_t off = 0;
+    cudaError_t reserve(size_t bytes) {  // every ring buffer holds `bytes` (sync callers only)
+        for (Buf& b : ring) {
+            if (b.cap >= bytes) continue;
+            if (b.done) {
+                cudaError_t e = cudaEventSynchronize(b.done);
+                if (e != cudaSuccess) return e;
+            }
+            if (b.host) cudaFreeHost(b.host);
+            b.host = nullptr;
+            b.cap = 0;
+            cudaError_t e = cudaMallocHost(&b.host, bytes);
+            if (e != cudaSuccess) return e;
+            b.cap = bytes;
+        }
+        return cudaSuccess;
+    }
     cudaError_t begin(cudaStream_t stream, bool use_async) {
         s = stream;
         async = use_async;
         off = 0;
-        if (async && done) return cudaEventSynchronize(done);  // the previous batch has been read
-        return cudaSuccess;
+        if (!async) return cudaSuccess;
+        cur = (cur + 1) % kRing;
+        // the buffer's previous batch was issued kRing batches ago: normally long done
+        return ring[cur].done ? cudaEventSynchronize(ring[cur].done) : cudaSuccess;
     }
     cudaError_t put(void* dst, const void* src, size_t bytes) {
         if (bytes == 0) return cudaSuccess;
         if (!async) return cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+        Buf& b = ring[cur];
         const size_t need = (off + bytes + 15) & ~size_t(15);
-        if (need > cap) {  // grow: earlier copies of this batch must have left the old buffer
+        if (need > b.cap) {  // beyond the bind-time bound: earlier copies must leave the old buffer
             cudaError_t e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) return e;
-            if (host) cudaFreeHost(host);
-            host = nullptr;
-            cap = std::max<size_t>(2 * need, 1 << 16);
-            e = cudaMallocHost(&host, cap);
-            if (e != cudaSuccess) { host = nullptr; cap = 0; return e; }
+            if (b.host) cudaFreeHost(b.host);
+            b.host = nullptr;
+            b.cap = std::max<size_t>(2 * need, 1 << 16);
+            e = cudaMallocHost(&b.host, b.cap);
+            if (e != cudaSuccess) { b.host = nullptr; b.cap = 0; return e; }
             off = 0;
         }
-        std::memcpy(host + off, src, bytes);
-        cudaError_t e = cudaMemcpyAsync(dst, host + off, bytes, cudaMemcpyHostToDevice, s);
+        std::memcpy(b.host + off, src, bytes);
+        cudaError_t e = cudaMemcpyAsync(dst, b.host + off, bytes, cudaMemcpyHostToDevice, s);
         off = (off + bytes + 15) & ~size_t(15);
         return e;
     }
@@ -134,18 +169,20 @@ struct Stager {
     }
     cudaError_t end() {
         if (!async) return cudaSuccess;
-        if (!done) {
-            cudaError_t e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        Buf& b = ring[cur];
+        if (!b.done) {
+            cudaError_t e = cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming);
             if (e != cudaSuccess) return e;
         }
-        return cudaEventRecord(done, s);
+        return cudaEventRecord(b.done, s);
     }
     void release() {
-        if (done) cudaEventDestroy(done);
-        if (host) cudaFreeHost(host);
-        done = nullptr;
-        host = nullptr;
-        cap = off = 0;
+        for (Buf& b : ring) {
+            if (b.done) cudaEventDestroy(b.done);
+            if (b.host) cudaFreeHost(b.host);
+            b = Buf{};
+        }
+        off = 0;
     }
 };
 
@@ -161,6 +198,13 @@ struct Layer {
     uint32_t batch = 0;
     std::vector<uint32_t> seq_lens;
     std::vector<UnitDesc> desc;
+    // Layout version: bumped whenever a kernel argument of the decode step (grids,
+    // work counts) changes; device arrays are capacity-reserved at bind, so their
+    // pointers never change between binds. Graphs captured over absp_decode_step stay
+    // valid while the version is unchanged (absp_layout_version).
+    uint64_t layout_version = 0;
+    uint64_t desc_version = 0;       // bumped by every layout (explicit work lists follow it)
+    std::vector<uint64_t> step_key;  // the step's kernel arguments that depend on the layout
     std::vector<ScoreItem> items;
     std::vector<uint32_t> item_begin;
     uint64_t total_cap = 0, total_centroids = 0;
@@ -183,7 +227,7 @@ struct Layer {
     DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
     DevBuf<float> qstat, qpart;     // frozen quantization statistics, build scratch
     DevBuf<uint32_t> wmask;         // decode-time maintenance: changed code words
-    DevBuf<float> part_o, part_ml;  // split-KV partials, sized by build_work
+    DevBuf<uint32_t> err_flags;     // explicit-selection validation (k_resolve_pages), kAttendErr*
     DevBuf<uint16_t> stage_q;
     DevBuf<float> stage_out;
     // absp_decode_step_host as one CUDA graph: H2D q -> step kernels -> D2H out; the
@@ -213,8 +257,7 @@ struct Layer {
         codes.release(); codes_min.release();
         sel_blocks.release(); sel_counts.release(); ready.release(); scored.release(); topk_units.release();
         approx.release(); unit_err.release();
-        part_o.release(); part_ml.release();
-        qstat.release(); qpart.release(); wmask.release();
+        qstat.release(); qpart.release(); wmask.release(); err_flags.release();
         stager.release();
         stage_q.release(); stage_out.release();
         drop_host_graph();
@@ -290,17 +333,27 @@ uint32_t chunks_for(uint32_t entries, uint32_t block) {
 
 // Builds the chunk list for units holding at most min(N, cap) entries (cap = K for
 // decode, blocks_stride for explicit selections), the CTA runs of every unit under
-// the persistent attention grid, and sizes the partial buffers.
+// the persistent attention grid, and sizes the list's buffers. With `reserve` the
+// buffers are sized for the layout at capacity (every unit at max_seq_len), so the
+// appends that grow the list later never reallocate: device pointers stay fixed from
+// kv_bind on (a unit's runs never exceed its chunks, so max_runs <= max chunks).
 absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t cap, int num_sms,
-                       WorkList& wl, Stager* up = nullptr) {
+                       WorkList& wl, Stager* up = nullptr, bool reserve = false) {
+    auto entries = [&](const UnitDesc& d, bool at_cap) {
+        return std::min(at_cap ? std::max(d.n_blocks, d.cap) : d.n_blocks, decode ? d.budget : cap);
+    };
     std::vector<uint32_t> base(l.desc.size() + 1, 0), unit_of, idx_of;
+    uint64_t n_work_cap = 0;
+    uint32_t max_chunks_cap = 1;
     for (size_t u = 0; u < l.desc.size(); ++u) {
         const UnitDesc& d = l.desc[u];
-        const uint32_t entries = std::min(d.n_blocks, decode ? d.budget : cap);
-        const uint32_t ch = std::max(chunks_for(entries, d.block), 1u);
+        const uint32_t ch = std::max(chunks_for(entries(d, false), d.block), 1u);
         base[u + 1] = base[u] + ch;
         unit_of.insert(unit_of.end(), ch, uint32_t(u));
         for (uint32_t c = 0; c < ch; ++c) idx_of.push_back(c);
+        const uint32_t ch_cap = std::max(chunks_for(entries(d, reserve), d.block), ch);
+        n_work_cap += ch_cap;
+        max_chunks_cap = std::max(max_chunks_cap, ch_cap);
     }
     wl.n_work = base.back();
     wl.ns = kAttnChunkRows / P;  // page slots per chunk
@@ -324,24 +377,28 @@ absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t c
     Stager sync_up;
     Stager& st = up ? *up : sync_up;
     const size_t n_slots = size_t(wl.n_work) * wl.ns;
-    ABSP_CUDA(wl.page.ensure(n_slots));
-    ABSP_CUDA(wl.valid.ensure(n_slots));
-    ABSP_CUDA(st.zero(wl.valid.p, n_slots * 2));
-    ABSP_CUDA(wl.chunk_unit.ensure(unit_of.size()));
-    ABSP_CUDA(wl.chunk_idx.ensure(idx_of.size()));
+    const size_t units = l.desc.size();
+    const size_t slots_res = std::max<size_t>(n_slots, size_t(n_work_cap) * wl.ns);
+    const size_t work_res = std::max<size_t>(wl.n_work, n_work_cap);
+    const size_t runs_res = reserve ? std::max(wl.max_runs, std::min(max_chunks_cap, uint32_t(num_sms))) : wl.max_runs;
+    const bool fresh = !wl.valid.p || wl.valid.n < slots_res;
+    ABSP_CUDA(wl.page.ensure(slots_res));
+    ABSP_CUDA(wl.valid.ensure(slots_res));
+    ABSP_CUDA(st.zero(wl.valid.p, (fresh ? slots_res : n_slots) * 2));
+    ABSP_CUDA(wl.chunk_unit.ensure(work_res));
+    ABSP_CUDA(wl.chunk_idx.ensure(work_res));
     ABSP_CUDA(wl.chunk_base.ensure(base.size()));
-    ABSP_CUDA(wl.unit_done.ensure(l.desc.size()));
-    ABSP_CUDA(wl.unit_run.ensure(l.desc.size()));
+    ABSP_CUDA(wl.unit_done.ensure(units));
+    ABSP_CUDA(wl.unit_run.ensure(units));
     ABSP_CUDA(st.put(wl.chunk_unit.p, unit_of.data(), unit_of.size() * 4));
     ABSP_CUDA(st.put(wl.chunk_idx.p, idx_of.data(), idx_of.size() * 4));
     ABSP_CUDA(st.put(wl.chunk_base.p, base.data(), base.size() * 4));
     ABSP_CUDA(st.put(wl.unit_run.p, run.data(), run.size() * 4));
-    ABSP_CUDA(st.zero(wl.unit_done.p, l.desc.size() * 4));
+    ABSP_CUDA(st.zero(wl.unit_done.p, units * 4));
     wl.h_base = base;
     wl.h_run = run;
-    // one partial slot per (unit, CTA run, consumer warp)
-    ABSP_CUDA(l.part_o.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 8 * D));
-    ABSP_CUDA(l.part_ml.ensure(l.desc.size() * size_t(wl.max_runs) * kAttnSplits * 16));
+    ABSP_CUDA(wl.part_o.ensure(units * runs_res * kAttnSplits * 8 * D));
+    ABSP_CUDA(wl.part_ml.ensure(units * runs_res * kAttnSplits * 16));
     return ABSP_OK;
 }
 
@@ -479,6 +536,14 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
         ABSP_CUDA(cudaMemset(l->scored.p, 0, units * 4));
     }
     Stager& up = l->stager;
+    if (!async) {  // bind: size the pinned upload ring for any later layout of this binding
+        size_t n_work_cap = 0;
+        for (const UnitDesc& d : l->desc)
+            n_work_cap += std::max(chunks_for(std::min(std::max(d.n_blocks, d.cap), d.budget), d.block), 1u);
+        const size_t bound = units * sizeof(UnitDesc) + (units + l->item_begin.size()) * sizeof(ScoreItem) +
+                             l->item_begin.size() * 4 + units * 4 * 3 + 2 * n_work_cap * 4 + 8 * 16 + 4096;
+        ABSP_CUDA(up.reserve(bound));
+    }
     ABSP_CUDA(up.begin(stream, async));
     // top-k classes: split only when the largest unit needs the big register variants
     l->topk_classes = TopkClasses{};
@@ -497,14 +562,23 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
         l->h_topk_order = order;
         l->topk_classes.units = l->topk_units.p;
     }
-    for (auto& kv : l->attend_work) kv.second.release();
-    l->attend_work.clear();
-    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work, &up);
+    // explicit-selection work lists are rebuilt (in place) by their next absp_attend
+    ++l->desc_version;
+    st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work, &up, /*reserve=*/true);
     if (st != ABSP_OK) return st;
     ABSP_CUDA(up.put(l->d_desc.p, l->desc.data(), units * sizeof(UnitDesc)));
     ABSP_CUDA(up.put(l->d_items.p, l->items.data(), l->items.size() * sizeof(ScoreItem)));
     ABSP_CUDA(up.put(l->d_item_begin.p, l->item_begin.data(), l->item_begin.size() * 4));
     ABSP_CUDA(up.end());
+    // the decode step's layout-dependent kernel arguments
+    std::vector<uint64_t> key = {l->step_work.n_work, l->step_work.grid, l->step_work.max_runs,
+                                 l->item_begin.size(), topk_items(l->max_nblocks), l->max_nblocks > 0,
+                                 uint64_t(l->topk_classes.units != nullptr)};
+    for (int cls = 0; cls <= kTopkClasses; ++cls) key.push_back(l->topk_classes.begin[cls]);
+    if (key != l->step_key) {
+        l->step_key = key;
+        ++l->layout_version;
+    }
     return ABSP_OK;
 }
 
@@ -716,11 +790,14 @@ absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const 
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "append kernel");
     for (uint32_t b = 0; b < l->batch; ++b) ++l->seq_lens[b];
-    l->drop_host_graph();
     // the grown layout is uploaded on the stream, after the append kernel and before
-    // the refresh (no host synchronisation; segments are capacity-reserved, so nothing moves)
+    // the refresh (no host synchronisation; segments and work lists are capacity-
+    // reserved, so nothing moves). The host-buffer step graph is re-captured only when
+    // a kernel argument of the step changed.
+    const uint64_t version = l->layout_version;
     st = layout_layer(ctx, l, s, true);
     if (st != ABSP_OK) return st;
+    if (l->layout_version != version) l->drop_host_graph();
     n = 0;
     e = launch_refresh_store(view_of(ctx, *l), l->max_cap, s, &n);
     ctx->launches += n;
@@ -754,7 +831,7 @@ static absp_status do_attend_step(absp_ctx* ctx, Layer* l, const void* q, float*
                                   cudaStream_t s) {
     int n = 0;
     cudaError_t e = launch_attend(view_of(ctx, *l), static_cast<const uint16_t*>(q), l->step_work.pages(), ready,
-                                  work_view(l->step_work), l->part_o.p, l->part_ml.p, out, s, &n);
+                                  work_view(l->step_work), l->step_work.part_o.p, l->step_work.part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
@@ -785,22 +862,26 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
     if (!q || !blocks || !counts || !out) return fail(ABSP_EINVAL, "attend: null pointer");
     if (blocks_stride == 0) return fail(ABSP_EINVAL, "attend: blocks_stride must be positive");
     DeviceGuard dg(ctx->device);
-    // Work list for selections of up to min(N, blocks_stride) entries per unit; built
-    // once per stride (the first call for a new stride allocates).
-    auto it = l->attend_work.find(blocks_stride);
-    if (it == l->attend_work.end()) {
-        st = build_work(*l, ctx->cfg.head_dim, ctx->cfg.page_size, false, blocks_stride, ctx->num_sms,
-                        l->attend_work[blocks_stride]);
+    // Work list (with its own partials) for selections of up to min(N, blocks_stride)
+    // entries per unit; built per stride on first use and rebuilt in place after the
+    // layout changed (an append). Building allocates / uploads synchronously.
+    WorkList& wl = l->attend_work[blocks_stride];
+    if (wl.layout != l->desc_version) {
+        st = build_work(*l, ctx->cfg.head_dim, ctx->cfg.page_size, false, blocks_stride, ctx->num_sms, wl);
         if (st != ABSP_OK) return st;
-        it = l->attend_work.find(blocks_stride);
+        wl.layout = l->desc_version;
+    }
+    if (!l->err_flags.p) {
+        ABSP_CUDA(l->err_flags.ensure(1));
+        ABSP_CUDA(cudaMemset(l->err_flags.p, 0, 4));
     }
     const LayerView v = view_of(ctx, *l);
     const cudaStream_t s = cudaStream_t(stream);
     int n = 0;
-    cudaError_t e = launch_resolve_pages(v, blocks, blocks_stride, counts, it->second.pages(), s, &n);
+    cudaError_t e = launch_resolve_pages(v, blocks, blocks_stride, counts, wl.pages(), l->err_flags.p, s, &n);
     if (e == cudaSuccess)
-        e = launch_attend(v, static_cast<const uint16_t*>(q), it->second.pages(), nullptr, work_view(it->second),
-                          l->part_o.p, l->part_ml.p, out, s, &n);
+        e = launch_attend(v, static_cast<const uint16_t*>(q), wl.pages(), nullptr, work_view(wl), wl.part_o.p,
+                          wl.part_ml.p, out, s, &n);
     ctx->launches += n;
     if (e != cudaSuccess) return cuda_fail(e, "attend kernels");
     return ABSP_OK;
@@ -815,6 +896,30 @@ absp_status absp_attend_selected(absp_ctx* ctx, uint32_t layer, const void* q, f
     if (!q || !out) return fail(ABSP_EINVAL, "attend_selected: null pointer");
     DeviceGuard dg(ctx->device);
     return do_attend_step(ctx, l, q, out, nullptr, cudaStream_t(stream));
+}
+
+absp_status absp_attend_validate(absp_ctx* ctx, uint32_t layer, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->err_flags.p) return ABSP_OK;  // no explicit attention yet
+    DeviceGuard dg(ctx->device);
+    const cudaStream_t s = cudaStream_t(stream);
+    uint32_t flags = 0;
+    ABSP_CUDA(cudaMemcpyAsync(&flags, l->err_flags.p, 4, cudaMemcpyDeviceToHost, s));
+    ABSP_CUDA(cudaMemsetAsync(l->err_flags.p, 0, 4, s));
+    ABSP_CUDA(cudaStreamSynchronize(s));
+    // the reference's messages (engine.cpp:224-226, kv_cache.cpp:125-127)
+    if (flags & kAttendErrEmpty) return fail(ABSP_EINVAL, "sparse_attention: empty selection for a head");
+    if (flags & kAttendErrCount) return fail(ABSP_EINVAL, "sparse_attention: selection count above blocks_stride");
+    if (flags & kAttendErrBlock) return fail(ABSP_ERANGE, "block_to_pages: block index out of range");
+    if (flags & kAttendErrPage) return fail(ABSP_ERANGE, "sparse_attention: page id outside the KV pools");
+    return ABSP_OK;
+}
+
+uint64_t absp_layout_version(absp_ctx* ctx, uint32_t layer) {
+    if (!ctx || layer >= ctx->layers.size()) return 0;
+    return ctx->layers[layer].layout_version;
 }
 
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,

@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, off);
-        const float inv = 1.0f / lpart;
+        const float inv = lpart > 0.0f ? 1.0f / lpart : 0.0f;  // an empty (rejected) selection writes zeros
         float* dst = out + (size_t(mu) * G + h) * D + lane * PER;  // out is [b][h*G + g][d], u = b*H + h
         if (PER == 4)
             *reinterpret_cast<float4*>(dst) = make_float4(acc[0] * inv, acc[1 % PER] * inv, acc[2 % PER] * inv,

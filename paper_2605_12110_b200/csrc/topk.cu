@@ -81,7 +81,7 @@ struct Keys {
     __device__ __forceinline__ uint32_t get(int j, uint32_t i) const {
         if (SMK) return sk[i];
         if (REG) return r[j];
-        return i < n_cand ? order_key(__ldg(sc + i)) : 0u;
+        return i < n_cand ? order_key(__ldcg(sc + i)) : 0u;
     }
     __device__ __forceinline__ uint32_t reg(int j, uint32_t warp, uint32_t lane) const {
         if (SMK) return sk[(j * kWarps + warp) * 32 + lane];
@@ -124,7 +124,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     const uint32_t nsteps = (n_cand + 31) / 32;
     const int my_items = REG ? ITEMS : int((nsteps + kWarps - 1 - warp) / kWarps);
 
-    griddep_launch_dependents();
     {   // the page resolution at the end reads the sequence's page-table row: the H units of
         // the sequence warm L2 with a slice each while the scores are being produced
         const uint32_t row_pages = (du.n_tokens + L.P - 1) / L.P;
@@ -145,7 +144,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     } else {
         griddep_wait();  // the scores are written by the scoring kernel of this step
     }
-    const float tail_score = N > K ? __ldg(sc + N - 1) : 0.0f;  // the trailing block, loaded early
+    // Only now may the attention kernel be scheduled. Its producers poll the per-unit
+    // ready flags without a grid dependency wait; the flags of the previous step are
+    // re-armed by that step's attention merges. Once every top-k CTA has seen its
+    // unit's scores, the scorer of this step has run past its own griddep_wait, i.e.
+    // the previous attention grid has completed and no stale flag is left to read.
+    griddep_launch_dependents();
+    const float tail_score = N > K ? __ldcg(sc + N - 1) : 0.0f;  // the trailing block, loaded early
     Keys<REG, ITEMS, SMK> keys;
     keys.sc = sc;
     keys.n_cand = n_cand;
@@ -155,13 +160,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
 #pragma unroll 16
         for (int j = 0; j < ITEMS; ++j) {
             const uint32_t i = (j * kWarps + warp) * 32 + lane;
-            topk_keys[i] = i < n_cand ? order_key(__ldg(sc + i)) : 0u;
+            topk_keys[i] = i < n_cand ? order_key(__ldcg(sc + i)) : 0u;
         }
     } else if (REG) {
 #pragma unroll
         for (int j = 0; j < (REG ? ITEMS : 1); ++j) {
             const uint32_t i = (j * kWarps + warp) * 32 + lane;
-            keys.r[j] = i < n_cand ? order_key(__ldg(sc + i)) : 0u;
+            keys.r[j] = i < n_cand ? order_key(__ldcg(sc + i)) : 0u;
         }
     }
     if (threadIdx.x == 0) {
@@ -523,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_topk(LayerView L, uint32_t* blo
     // ---- gather the winners -------------------------------------------------
     if (N <= K) {
         for (uint32_t i = threadIdx.x; i < N; i += kThreads)
-            sm.sel[i] = (uint64_t(order_key(sc[i])) << 32) | uint32_t(~i);
+            sm.sel[i] = (uint64_t(order_key(__ldcg(sc + i))) << 32) | uint32_t(~i);
     } else {
         const uint32_t tau = sm.state[0];
         const uint32_t need_eq = sm.state[2];
@@ -719,9 +724,14 @@ cudaError_t launch_topk(const LayerView& L, uint32_t max_nblocks, uint32_t max_b
     return cudaGetLastError();
 }
 
-// Page resolution for an explicit (caller-provided) selection: absp_attend.
+// Page resolution for an explicit (caller-provided) selection: absp_attend. The
+// selection is validated as the reference's check_selection / block_to_pages do
+// (engine.cpp:212-232, kv_cache.cpp:118-138): an empty selection, a count above
+// blocks_stride, a block id past the unit's blocks or a page-table entry outside the
+// pools raises a bit of *err (read back by absp_attend_validate); offending entries
+// are dropped, so no copy leaves the K/V pools.
 __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks, uint32_t stride,
-                                const uint32_t* __restrict__ counts, PageList pages) {
+                                const uint32_t* __restrict__ counts, PageList pages, uint32_t* err) {
     griddep_launch_dependents();
     griddep_wait();  // blocks / counts may come from the previous kernel
     const uint32_t u = blockIdx.x;
@@ -729,7 +739,13 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
     const uint32_t ppb = du.block / L.P;
     const uint32_t E = kAttnChunkRows / du.block;
     const uint32_t cap = min(stride, du.n_blocks);  // entries the work list reserves
-    const uint32_t cnt = min(counts[u], cap);
+    const uint32_t raw = counts[u];
+    const uint32_t cnt = min(raw, cap);
+    uint32_t flags = 0;
+    if (threadIdx.x == 0) {
+        if (raw == 0) flags |= kAttendErrEmpty;
+        if (raw > stride) flags |= kAttendErrCount;
+    }
     const uint32_t slot_end = ((cap + E - 1) / E) * E * ppb;
     const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
     const uint32_t head_base = du.head * uint32_t(L.pool_pages);
@@ -738,20 +754,31 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
         const uint32_t e = s / ppb, pp = s % ppb;
         uint32_t v = 0, page = 0;
         if (e < cnt) {
-            const uint32_t t0 = __ldg(blocks + size_t(u) * stride + e) * du.block + pp * L.P;
-            if (t0 < du.n_tokens) {
-                v = min(L.P, du.n_tokens - t0);
-                page = head_base + __ldg(pt + t0 / L.P);
+            const uint32_t blk = __ldg(blocks + size_t(u) * stride + e);
+            if (blk >= du.n_blocks) {
+                flags |= kAttendErrBlock;
+            } else {
+                const uint32_t t0 = blk * du.block + pp * L.P;
+                if (t0 < du.n_tokens) {
+                    const uint32_t pid = __ldg(pt + t0 / L.P);
+                    if (pid >= L.pool_pages) {
+                        flags |= kAttendErrPage;
+                    } else {
+                        v = min(L.P, du.n_tokens - t0);
+                        page = head_base + pid;
+                    }
+                }
             }
         }
         pages.page[base + s] = page;
         pages.valid[base + s] = uint16_t(v);
     }
+    if (flags && err) atomicOr(err, flags);
 }
 cudaError_t launch_resolve_pages(const LayerView& L, const uint32_t* blocks, uint32_t stride,
-                                 const uint32_t* counts, const PageList& pages, cudaStream_t s,
+                                 const uint32_t* counts, const PageList& pages, uint32_t* err, cudaStream_t s,
                                  int* launches) {
-    launch_pdl(k_resolve_pages, dim3(L.units), dim3(256), 0, s, L, blocks, stride, counts, pages);
+    launch_pdl(k_resolve_pages, dim3(L.units), dim3(256), 0, s, L, blocks, stride, counts, pages, err);
     ++*launches;
     return cudaGetLastError();
 }
