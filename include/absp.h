@@ -253,6 +253,47 @@ absp_status absp_fill_synthetic_bf16(void* dst, uint64_t count, uint64_t seed,
  * (benchmark accounting). */
 uint64_t absp_launch_count(absp_ctx* ctx);
 
+/* ---------------------------------------------------------------------------
+ * DecodeEngine (engine.hpp:90-129, engine.cpp:405-463) for one sequence, with no
+ * caller-side device memory: the engine owns its paged bf16 KV cache (per-head pools,
+ * sequential page ids as kv_cache.cpp:53-60 hands out), a one-layer context, a stream
+ * and pinned staging buffers. Host fp32 in, host fp32 out; inputs are stored as bf16
+ * (RNE), all arithmetic runs in the sm_100a kernels.
+ * ------------------------------------------------------------------------- */
+typedef struct absp_engine absp_engine;
+
+/* DecodeEngine::DecodeEngine(config, assignment, capacity_tokens): validates the config
+ * (EngineConfig::validate) and the per-KV-head block sizes (BlockAssignment::validate);
+ * cfg->max_batch / max_seq_len / num_layers are replaced by 1 / capacity / 1. */
+absp_status absp_engine_create(int device, const absp_config* cfg, const uint32_t* block_sizes,
+                               uint64_t capacity_tokens, absp_engine** out);
+absp_status absp_engine_destroy(absp_engine* engine);
+
+/* DecodeEngine::prefill (engine.cpp:414-440): keys / values are host spans of
+ * keys_len / values_len floats, head-major [H][tokens][d] with head h starting at
+ * h * (len / H); the first num_tokens tokens of every head are cached, then the
+ * centroid store is built and quantized. ESTATE if already prefilled, EINVAL if a
+ * span is smaller than num_tokens, ECAPACITY above the capacity. Synchronous. */
+absp_status absp_engine_prefill(absp_engine* engine, const float* keys, uint64_t keys_len, const float* values,
+                                uint64_t values_len, uint64_t num_tokens);
+
+/* DecodeEngine::step (engine.cpp:442-463): appends keys / values ([H][d] host fp32),
+ * maintains the store (refresh_tail_centroids + requantize_heads), then estimate ->
+ * select -> attend for `query` ([Hq][d] host fp32). Writes out [Hq][d] (host fp32),
+ * the ordered selection per KV head (blocks [H][blocks_stride] and counts [H], host;
+ * either may be NULL) and whether seq_len <= token_budget (the reference's full-
+ * attention fallback: every block is then selected and attended). ESTATE before
+ * prefill, EINVAL on a size mismatch, ECAPACITY at capacity. Synchronous. */
+absp_status absp_engine_step(absp_engine* engine, const float* keys, uint64_t keys_len, const float* values,
+                             uint64_t values_len, const float* query, uint64_t query_len, float* out,
+                             uint32_t* blocks, uint32_t blocks_stride, uint32_t* counts,
+                             int* full_attention_fallback);
+
+/* Current sequence length, the minimal blocks_stride (ceil(T / min block size)) and the
+ * engine's context (layer 0), e.g. for absp_download_store (DecodeEngine::centroids /
+ * quantized). */
+absp_status absp_engine_info(absp_engine* engine, uint64_t* seq_len, uint32_t* blocks_stride, absp_ctx** ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,8 @@
  *     store read back in the reference layouts)      centroids.hpp:31-52, quantizer.hpp:18-38
  *   BlockAssignment::load / save                   <- read/write_assignment_file
  *                                                     calibrator.cpp:277-311
+ *   absp::DecodeEngine / StepResult               <- DecodeEngine (engine.hpp:84-129): owns its
+ *                                                    device cache, store and stream (absp_engine_*)
  *   absp::DecodeAttention                         <- the device replacement of
  *     build_store   = compute_block_centroids + quantize_store (centroids.hpp:56-57,
  *                                                              quantizer.hpp:43)
@@ -360,6 +362,118 @@ class DecodeAttention {
   private:
     EngineConfig config_;
     absp_ctx* ctx_ = nullptr;
+};
+
+// StepResult (engine.hpp:84-88): the attention output [Hq][d], the ordered selection
+// per KV head (SelectionResult::blocks) and whether the reference would have used its
+// full-attention fallback (seq_len <= token_budget; every block is then selected).
+struct StepResult {
+    std::vector<float> output;
+    std::vector<std::vector<std::size_t>> blocks;
+    bool full_attention_fallback = false;
+};
+
+// DecodeEngine (engine.hpp:90-129, engine.cpp:405-463) for one sequence on one GPU:
+// owns its paged bf16 KV cache, quantized centroid store and stream (absp_engine_*),
+// with the reference's constructor, prefill and step signatures (spans as pointer +
+// length) and exceptions. centroids() / quantized() return host snapshots of the device
+// store in the reference layouts (CentroidStore / QuantizedCentroidStore).
+class DecodeEngine {
+  public:
+    DecodeEngine(const EngineConfig& config, const BlockAssignment& assignment, std::size_t capacity_tokens,
+                 int device = 0)
+        : config_(config), assignment_(assignment) {
+        config_.validate();
+        assignment_.validate(config_);
+        const absp_config c = config_.to_abi();
+        std::vector<uint32_t> b(assignment_.block_sizes.begin(), assignment_.block_sizes.end());
+        check(absp_engine_create(device, &c, b.data(), capacity_tokens, &eng_));
+        absp_ctx* ctx = nullptr;
+        check(absp_engine_info(eng_, nullptr, &stride_, &ctx));
+    }
+    ~DecodeEngine() { absp_engine_destroy(eng_); }
+    DecodeEngine(const DecodeEngine&) = delete;
+    DecodeEngine& operator=(const DecodeEngine&) = delete;
+
+    // keys / values head-major [head][token][channel] (engine.hpp:102-105)
+    void prefill(const float* keys, std::size_t keys_len, const float* values, std::size_t values_len,
+                 std::size_t num_tokens) {
+        check(absp_engine_prefill(eng_, keys, keys_len, values, values_len, num_tokens));
+    }
+    void prefill(const std::vector<float>& keys, const std::vector<float>& values, std::size_t num_tokens) {
+        prefill(keys.data(), keys.size(), values.data(), values.size(), num_tokens);
+    }
+    // keys / values: num_heads * head_dim floats; query: num_q_heads * head_dim floats
+    StepResult step(const float* keys, std::size_t keys_len, const float* values, std::size_t values_len,
+                    const float* query, std::size_t query_len) {
+        const std::size_t H = config_.num_heads;
+        const std::size_t Hq = config_.num_q_heads ? config_.num_q_heads : H;
+        StepResult r;
+        r.output.resize(Hq * config_.head_dim);
+        std::vector<uint32_t> blocks(H * stride_), counts(H);
+        int fb = 0;
+        check(absp_engine_step(eng_, keys, keys_len, values, values_len, query, query_len, r.output.data(),
+                               blocks.data(), stride_, counts.data(), &fb));
+        r.blocks.resize(H);
+        for (std::size_t h = 0; h < H; ++h)
+            r.blocks[h].assign(blocks.begin() + h * stride_, blocks.begin() + h * stride_ + counts[h]);
+        r.full_attention_fallback = fb != 0;
+        return r;
+    }
+    StepResult step(const std::vector<float>& keys, const std::vector<float>& values,
+                    const std::vector<float>& query) {
+        return step(keys.data(), keys.size(), values.data(), values.size(), query.data(), query.size());
+    }
+
+    const EngineConfig& config() const { return config_; }
+    const BlockAssignment& assignment() const { return assignment_; }
+    std::size_t seq_len() const {
+        uint64_t n = 0;
+        check(absp_engine_info(eng_, &n, nullptr, nullptr));
+        return std::size_t(n);
+    }
+    // CentroidStore (+ QuantizedCentroidStore when quantized) of the sequence.
+    StoreSnapshot centroids() const { return snapshot(); }
+    std::optional<StoreSnapshot> quantized() const {
+        if (!config_.quant) return std::nullopt;
+        return snapshot();
+    }
+    absp_engine* handle() const { return eng_; }
+
+  private:
+    StoreSnapshot snapshot() const {
+        absp_ctx* ctx = nullptr;
+        check(absp_engine_info(eng_, nullptr, nullptr, &ctx));
+        const std::size_t H = config_.num_heads, d = config_.head_dim;
+        std::vector<uint64_t> off(H + 1);
+        check(absp_download_store(ctx, 0, 0, off.data(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, nullptr));
+        StoreSnapshot s;
+        s.offsets.assign(off.begin(), off.end());
+        const std::size_t n = s.total_centroids();
+        const bool mm = config_.centroid_method == CentroidMethod::kMaxMin;
+        s.values.resize(n * d);
+        if (mm) s.values_min.resize(n * d);
+        if (config_.quant) {
+            s.codes.resize(n * d);
+            s.scales.resize(H * d);
+            s.zero_points.resize(H * d);
+            if (mm) {
+                s.codes_min.resize(n * d);
+                s.scales_min.resize(H * d);
+                s.zero_points_min.resize(H * d);
+            }
+        }
+        auto p = [](auto& v) { return v.empty() ? nullptr : v.data(); };
+        check(absp_download_store(ctx, 0, 0, nullptr, p(s.values), p(s.values_min), p(s.codes), p(s.codes_min),
+                                  p(s.scales), p(s.zero_points), p(s.scales_min), p(s.zero_points_min)));
+        return s;
+    }
+
+    EngineConfig config_;
+    BlockAssignment assignment_;
+    absp_engine* eng_ = nullptr;
+    uint32_t stride_ = 0;
 };
 
 }  // namespace absp

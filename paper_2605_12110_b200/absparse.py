@@ -403,72 +403,81 @@ class StepResult:
 
 
 class DecodeEngine:
-    """DecodeEngine (engine.hpp:90-129, engine.cpp:405-463) on the GPU for one sequence.
-
-    Owns the paged bf16 KV cache (per-head pools, page ids handed out sequentially as
-    kv_cache.cpp:53-60 does), the quantized store, and runs prefill / step through the
-    C ABI: step = absp_append (append + refresh_tail_centroids + requantize_heads) +
-    absp_decode_step (estimate -> select -> attend). With seq_len <= token_budget every
+    """DecodeEngine (engine.hpp:90-129, engine.cpp:405-463) on the GPU for one sequence,
+    over the library's engine object (absp_engine_*, no PyTorch): it owns the paged bf16
+    KV cache (per-head pools, page ids handed out sequentially as kv_cache.cpp:53-60
+    does), the quantized store and a stream. step = append + refresh_tail_centroids +
+    requantize_heads + estimate -> select -> attend. With seq_len <= token_budget every
     block is selected, so the sparse output is the full attention the reference falls
-    back to (engine.cpp:456-458). Inputs are fp32 and stored as bf16.
-    """
+    back to (engine.cpp:456-458). Inputs are fp32 and stored as bf16."""
 
     def __init__(self, config: EngineConfig, assignment: BlockAssignment, capacity_tokens: int, device: int = 0):
-        import torch
         assignment.validate(config)
+        if config.quant is not None:
+            config.quant.validate()
         cfg = EngineConfig(**{**config.__dict__, "max_batch": 1, "max_seq_len": int(capacity_tokens),
                               "num_layers": 1})
         self.config = cfg
         self.assignment = assignment
-        self._torch = torch
-        self._dev = torch.device("cuda", device)
-        self.da = DecodeAttention(cfg, device=device)
-        self.da.set_assignment(0, assignment)
-        H, d, P = cfg.num_heads, cfg.head_dim, cfg.page_size
-        self._pages = (int(capacity_tokens) + P - 1) // P
-        self.k_pool = torch.zeros(H, self._pages, P, d, dtype=torch.int16, device=self._dev)
-        self.v_pool = torch.zeros_like(self.k_pool)
-        self.page_table = torch.arange(self._pages, dtype=torch.int32, device=self._dev).reshape(1, -1)
-        self.seq_len = 0
-        self._prefilled = False
+        self._lib = _abi.load()
+        self._eng = C.c_void_p()
+        bs = (C.c_uint32 * len(assignment.block_sizes))(*assignment.block_sizes)
+        check(self._lib.absp_engine_create(device, C.byref(cfg.to_abi()), bs, int(capacity_tokens),
+                                           C.byref(self._eng)))
+        ctx, stride = C.c_void_p(), C.c_uint32()
+        check(self._lib.absp_engine_info(self._eng, None, C.byref(stride), C.byref(ctx)))
+        self._stride = stride.value
+        # the engine's context, for store / selection read-back (owned by the engine)
+        self.da = DecodeAttention.__new__(DecodeAttention)
+        self.da.config, self.da.device, self.da._lib, self.da._ctx = cfg, device, self._lib, ctx
+        self.da._seq_lens = {0: [0]}
+        self.da.close = lambda: None
+
+    def close(self) -> None:
+        if self._eng:
+            self._lib.absp_engine_destroy(self._eng)
+            self._eng = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def seq_len(self) -> int:
+        n = C.c_uint64()
+        check(self._lib.absp_engine_info(self._eng, C.byref(n), None, None))
+        return int(n.value)
 
     def prefill(self, keys, values, num_tokens: int) -> None:
-        """keys / values: [H][tokens][d] fp32, the first num_tokens tokens are cached."""
-        if self._prefilled:
-            raise LogicError("prefill: engine already prefilled")
-        cfg = self.config
-        H, d, P = cfg.num_heads, cfg.head_dim, cfg.page_size
-        k = np.asarray(keys, np.float32).reshape(H, -1, d)
-        v = np.asarray(values, np.float32).reshape(H, -1, d)
-        if num_tokens == 0 or k.shape[1] < num_tokens or v.shape[1] < num_tokens:
-            raise InvalidArgument("prefill: tensor smaller than num_tokens")
-        if num_tokens > cfg.max_seq_len:
-            raise CapacityError(f"append: kv cache at capacity ({cfg.max_seq_len} tokens)")
-        pages = (num_tokens + P - 1) // P
-        for pool, src in ((self.k_pool, k), (self.v_pool, v)):
-            buf = np.zeros((H, pages * P, d), np.uint16)
-            buf[:, :num_tokens] = _to_bf16_bits(src[:, :num_tokens])
-            pool[:, :pages] = self._torch.from_numpy(buf.view(np.int16).reshape(H, pages, P, d)).to(self._dev)
-        self.da.bind(0, self.k_pool, self.v_pool, self.page_table, [num_tokens])
-        self.da.build_store(0)
-        self.seq_len = num_tokens
-        self._prefilled = True
+        """keys / values: head-major [H][tokens][d] fp32 (engine.hpp:102-105)."""
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        check(self._lib.absp_engine_prefill(self._eng, k.ctypes.data, k.size, v.ctypes.data, v.size,
+                                            int(num_tokens)))
+        self.da._seq_lens[0] = [self.seq_len]
 
     def step(self, keys, values, query) -> StepResult:
         """keys / values: [H][d] fp32 of the new token; query: [Hq][d] fp32."""
-        if not self._prefilled:
-            raise LogicError("step: call prefill first")
-        cfg = self.config
-        H, d = cfg.num_heads, cfg.head_dim
-        Hq = cfg.num_q_heads or H
-        torch = self._torch
-        kn = torch.from_numpy(_to_bf16_bits(np.asarray(keys).reshape(1, H, d)).view(np.int16)).to(self._dev)
-        vn = torch.from_numpy(_to_bf16_bits(np.asarray(values).reshape(1, H, d)).view(np.int16)).to(self._dev)
-        q = torch.from_numpy(_to_bf16_bits(np.asarray(query).reshape(1, Hq, d)).view(np.int16)).to(self._dev)
-        self.da.append(0, kn, vn)
-        self.seq_len += 1
-        out = torch.empty(1, Hq, d, dtype=torch.float32, device=self._dev)
-        self.da.decode_step(0, q, out)
-        torch.cuda.synchronize(self._dev)
-        sel = self.da.download_selection(0)[0]
-        return StepResult(out[0].cpu().numpy(), sel, self.seq_len <= cfg.token_budget)
+        H, d = self.config.num_heads, self.config.head_dim
+        Hq = self.config.num_q_heads or H
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        q = np.ascontiguousarray(query, np.float32)
+        out = np.zeros((Hq, d), np.float32)
+        blocks = np.zeros((H, self._stride), np.uint32)
+        counts = np.zeros(H, np.uint32)
+        fb = C.c_int()
+        check(self._lib.absp_engine_step(self._eng, k.ctypes.data, k.size, v.ctypes.data, v.size, q.ctypes.data,
+                                         q.size, out.ctypes.data, blocks.ctypes.data, self._stride,
+                                         counts.ctypes.data, C.byref(fb)))
+        self.da._seq_lens[0] = [self.seq_len]
+        return StepResult(out, [blocks[h, :counts[h]].copy() for h in range(H)], bool(fb.value))
+
+    def centroids(self) -> dict:
+        """CentroidStore (+ QuantizedCentroidStore) of the sequence, reference layouts."""
+        return self.da.download_store(0, 0)
+
+    def quantized(self):
+        return self.da.download_store(0, 0) if self.config.quant is not None else None

@@ -11,6 +11,9 @@
 
 namespace absp {
 
+// The thread-local message absp_last_error() returns (api.cu).
+void set_last_error(const std::string& msg);
+
 // ---------------------------------------------------------------------------
 // Per-(sequence, KV head) "unit" metadata, device-resident, one array per layer.
 // A unit is the reference's per-head segment of one sequence

@@ -269,6 +269,8 @@ struct Layer {
 
 }  // namespace
 
+void absp::set_last_error(const std::string& msg) { g_err = msg; }
+
 struct absp_ctx {
     int device = 0;
     int num_sms = 148;

@@ -95,3 +95,6 @@ def test_no_cpu_fallback_without_gpu():
     from paper_2605_12110_b200 import DecodeAttention
     with pytest.raises(_abi.CudaError):
         DecodeAttention(_cfg())
+    from paper_2605_12110_b200 import BlockAssignment, DecodeEngine
+    with pytest.raises(_abi.CudaError):  # the engine object has no CPU path either
+        DecodeEngine(_cfg(max_batch=1), BlockAssignment.cycled(8, (16, 32, 64)), 4096)
