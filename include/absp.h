@@ -235,10 +235,13 @@ absp_status absp_download_store(absp_ctx* ctx, uint32_t layer, uint32_t seq, uin
  * like estimate_scores' output (fp32 [total]); synchronous. */
 absp_status absp_download_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* scores);
 
-/* Diagnostics of absp_decode_step's selection filter (INT4 mean stores, select.cu):
- * the approximate scores of one sequence (fp32 [total], estimate_scores layout) and
- * the per-KV-head error bound E_h with |approx - exact| <= E_h; synchronous. Only
- * meaningful after a decode step that used the filter. */
+/* Diagnostics of absp_decode_step's fused selection (INT4 mean stores, select.cu):
+ * with diagnostics enabled for the layer, decode steps also store every centroid's
+ * approximate score A_i (the linearised score up to a per-unit constant) and the
+ * per-unit bound E with |S_i - C_u - A_i| <= E (S_i the exact score). Off by default. */
+absp_status absp_set_filter_diagnostics(absp_ctx* ctx, uint32_t layer, int enable);
+/* One sequence's approximate scores (fp32 [total], estimate_scores layout) and the
+ * per-KV-head bounds E_h of the last diagnostic decode step; synchronous. */
 absp_status absp_download_filter_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* approx,
                                         float* err);
 

@@ -29,7 +29,7 @@ EXPORTED = [
     "absp_ctx_destroy", "absp_set_assignment", "absp_kv_bind", "absp_build_store", "absp_append", "absp_select",
     "absp_attend", "absp_attend_selected", "absp_decode_step", "absp_decode_step_host", "absp_last_selection",
     "absp_get_layer_info", "absp_download_store", "absp_download_scores", "absp_download_selection", "absp_download_filter_scores",
-    "absp_fill_synthetic_bf16", "absp_launch_count", "absp_attend_validate", "absp_layout_version",
+    "absp_fill_synthetic_bf16", "absp_launch_count", "absp_attend_validate", "absp_layout_version", "absp_set_filter_diagnostics",
     "absp_engine_create", "absp_engine_destroy", "absp_engine_prefill", "absp_engine_step", "absp_engine_info",
 ]
 
@@ -131,6 +131,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
     L.absp_download_filter_scores.argtypes = [vp, u32, u32, vp, vp]
     L.absp_fill_synthetic_bf16.argtypes = [vp, u64, u64, u64, vp]
     L.absp_attend_validate.argtypes = [vp, u32, vp]
+    L.absp_set_filter_diagnostics.argtypes = [vp, u32, C.c_int]
     L.absp_layout_version.argtypes = [vp, u32]
     L.absp_layout_version.restype = u64
     L.absp_engine_create.argtypes = [C.c_int, C.POINTER(Config), u32p, u64, C.POINTER(vp)]

@@ -329,6 +329,10 @@ class DecodeAttention:
         check(self._lib.absp_download_selection(self._ctx, layer, blocks.ctypes.data, counts.ctypes.data))
         return [[blocks[b, h, :counts[b, h]].copy() for h in range(H)] for b in range(batch)]
 
+    def set_filter_diagnostics(self, layer: int, enable: bool = True) -> None:
+        """Decode steps also store the fused selection's approximate scores and bounds."""
+        check(self._lib.absp_set_filter_diagnostics(self._ctx, layer, int(enable)))
+
     def download_filter_scores(self, layer: int, seq: int):
         """(approximate scores [total], per-KV-head error bounds [H]) of the decode step's
         selection filter for one sequence (diagnostics)."""

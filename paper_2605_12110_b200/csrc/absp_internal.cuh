@@ -172,13 +172,23 @@ cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList&
                           const AttendWork& work, float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches);
 size_t attend_smem_bytes(uint32_t D, uint32_t P);
-// Decode-step selection via tensor-core filter + exact refine (select.cu): same
-// ordered selections as launch_score + launch_topk, without full exact scores.
-bool select_fast_supported(const LayerView& L, uint32_t max_nblocks, uint32_t max_budget);
+// Fused decode-step selection (select.cu): estimate + select + page resolution per
+// (sequence, KV head) unit in one kernel, one cluster of `cluster` CTAs per unit; the
+// same ordered selections as launch_score + launch_topk (INT4 mean stores).
+bool select_fused_supported(const LayerView& L);
+struct SelectPlan {
+    uint32_t cluster;    // CTAs per unit (thread-block cluster size)
+    uint32_t stages;     // code-ring stages (2..4)
+    uint32_t slice_cap;  // key slots per CTA (largest unit at capacity / cluster)
+    uint32_t cand_cap;   // candidates the leader orders
+    bool ok;             // fits in shared memory
+};
+SelectPlan plan_select(uint32_t units, uint32_t max_cap_blocks, uint32_t max_budget, uint32_t D, int num_sms);
+size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t slice_cap, uint32_t cand_cap);
 cudaError_t init_select_attributes();  // per device, once
-cudaError_t launch_select_fast(const LayerView& L, const uint16_t* q, const ScoreWork& work, float* approx,
-                               float* err, uint32_t* blocks, uint32_t stride, uint32_t* counts,
-                               const PageList& pages, uint32_t* ready, cudaStream_t s, int* launches);
+cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, uint32_t* blocks,
+                                uint32_t stride, uint32_t* counts, const PageList& pages, uint32_t* ready,
+                                float* diag_approx, float* diag_err, cudaStream_t s, int* launches);
 cudaError_t init_attend_attributes();  // per device, once
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);

@@ -224,7 +224,9 @@ struct Layer {
     DevBuf<uint32_t> topk_units;  // units grouped by top-k register class
     std::vector<uint32_t> h_topk_order;
     TopkClasses topk_classes{};
-    DevBuf<float> approx, unit_err;  // decode-step filter: approximate scores, per-unit bounds
+    DevBuf<float> approx, unit_err;  // decode-step filter diagnostics: approximate scores, per-unit bounds
+    bool filter_diag = false;        // the fused selection writes them (absp_set_filter_diagnostics)
+    SelectPlan sel_plan{};           // fused selection: cluster size, ring stages, capacities
     DevBuf<float> qstat, qpart;     // frozen quantization statistics, build scratch
     DevBuf<uint32_t> wmask;         // decode-time maintenance: changed code words
     DevBuf<uint32_t> err_flags;     // explicit-selection validation (k_resolve_pages), kAttendErr*
@@ -274,7 +276,7 @@ void absp::set_last_error(const std::string& msg) { g_err = msg; }
 struct absp_ctx {
     int device = 0;
     int num_sms = 148;
-    bool fast_select = false;  // ABSP_FAST_SELECT=1: decode steps select through select.cu
+    bool exact_select = false;  // ABSP_EXACT_SELECT=1: decode steps use the full exact scorer + top-k
     absp_config cfg{};
     std::vector<Layer> layers;
     uint64_t launches = 0;
@@ -528,6 +530,11 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
     ABSP_CUDA(l->scores.ensure(l->total_cap));
     ABSP_CUDA(l->approx.ensure(l->total_cap));
     ABSP_CUDA(l->unit_err.ensure(units));
+    {
+        uint32_t max_cap_blocks = 0;
+        for (const UnitDesc& d : l->desc) max_cap_blocks = std::max(max_cap_blocks, d.cap);
+        l->sel_plan = plan_select(uint32_t(units), max_cap_blocks, l->max_budget, c.head_dim, ctx->num_sms);
+    }
     l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
     ABSP_CUDA(l->sel_counts.ensure(units));
@@ -666,8 +673,8 @@ absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) 
     auto* ctx = new absp_ctx;
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
-    const char* fs = std::getenv("ABSP_FAST_SELECT");
-    ctx->fast_select = fs && fs[0] == '1';
+    const char* es = std::getenv("ABSP_EXACT_SELECT");
+    ctx->exact_select = es && es[0] == '1';
     ctx->cfg = *cfg;
     ctx->layers.resize(cfg->num_layers);
     *out = ctx;
@@ -934,14 +941,15 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     DeviceGuard dg(ctx->device);
     const cudaStream_t s = cudaStream_t(stream);
     const LayerView v = view_of(ctx, *l);
-    if (ctx->fast_select && select_fast_supported(v, l->max_nblocks, l->max_budget)) {
-        const ScoreWork sw{l->d_items.p, l->d_item_begin.p, uint32_t(l->item_begin.size() - 1), nullptr};
+    if (!ctx->exact_select && select_fused_supported(v) && l->sel_plan.ok) {
+        // fused filter + exact refine + top-k + page resolution, one cluster per unit
         int n = 0;
-        cudaError_t e = launch_select_fast(v, static_cast<const uint16_t*>(q), sw, l->approx.p, l->unit_err.p,
-                                           l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->step_work.pages(),
-                                           l->ready.p, s, &n);
+        cudaError_t e = launch_select_fused(v, static_cast<const uint16_t*>(q), l->sel_plan, l->sel_blocks.p,
+                                            l->sel_stride, l->sel_counts.p, l->step_work.pages(), l->ready.p,
+                                            l->filter_diag ? l->approx.p : nullptr,
+                                            l->filter_diag ? l->unit_err.p : nullptr, s, &n);
         ctx->launches += n;
-        if (e != cudaSuccess) return cuda_fail(e, "select kernels");
+        if (e != cudaSuccess) return cuda_fail(e, "select kernel");
     } else {
         st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->ready.p, s);
         if (st != ABSP_OK) return st;
@@ -1175,6 +1183,15 @@ absp_status absp_download_selection(absp_ctx* ctx, uint32_t layer, uint32_t* blo
     const size_t units = l->desc.size();
     ABSP_CUDA(cudaMemcpy(blocks, l->sel_blocks.p, units * l->sel_stride * 4, cudaMemcpyDeviceToHost));
     ABSP_CUDA(cudaMemcpy(counts, l->sel_counts.p, units * 4, cudaMemcpyDeviceToHost));
+    return ABSP_OK;
+}
+
+absp_status absp_set_filter_diagnostics(absp_ctx* ctx, uint32_t layer, int enable) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    l->filter_diag = enable != 0;
+    l->drop_host_graph();
     return ABSP_OK;
 }
 

@@ -19,8 +19,9 @@ def to_dev_u32(a: np.ndarray) -> torch.Tensor:
 
 
 class GpuLayer:
-    def __init__(self, layer, T, method=0, bits=4, mode=1, max_seq_len=None, candidates=None, fast=False):
-        """fast=True: decode steps select through select.cu (ABSP_FAST_SELECT=1)."""
+    def __init__(self, layer, T, method=0, bits=4, mode=1, max_seq_len=None, candidates=None, exact_select=False):
+        """exact_select=True: decode steps score every centroid exactly and run the separate
+        top-k (ABSP_EXACT_SELECT=1) instead of the fused filter + refine (select.cu)."""
         self.layer = layer
         cands = sorted(set(candidates or layer.block_sizes))
         self.cfg = EngineConfig(num_heads=layer.H, head_dim=layer.d, page_size=layer.P,
@@ -29,15 +30,15 @@ class GpuLayer:
                                 quant=QuantSpec(bits, QuantMode(mode)) if bits else None,
                                 num_q_heads=layer.H * layer.G, max_batch=layer.batch,
                                 max_seq_len=max_seq_len or max(layer.seq_lens), num_layers=1)
-        old = os.environ.get("ABSP_FAST_SELECT")
-        os.environ["ABSP_FAST_SELECT"] = "1" if fast else "0"
+        old = os.environ.get("ABSP_EXACT_SELECT")
+        os.environ["ABSP_EXACT_SELECT"] = "1" if exact_select else "0"
         try:
             self.da = DecodeAttention(self.cfg)
         finally:
             if old is None:
-                del os.environ["ABSP_FAST_SELECT"]
+                del os.environ["ABSP_EXACT_SELECT"]
             else:
-                os.environ["ABSP_FAST_SELECT"] = old
+                os.environ["ABSP_EXACT_SELECT"] = old
         self.da.set_assignment(0, BlockAssignment(list(layer.block_sizes)))
         self.k = to_dev_u16(layer.k_pool)
         self.v = to_dev_u16(layer.v_pool)
