@@ -305,12 +305,23 @@ def verify_layer(da, l, lay, b, w, Hl, bs_local):
     qb = O.bf16_to_f32(lay["q"][b].cpu().numpy().view(np.uint16)).reshape(Hl * G, d)
     qsum = O.group_sum(qb, Hl, G)
     sc = ref.scores(qsum)
+    import torch
+    info = da.layer_info(l)
+    Bl = lay["q"].shape[0]
+    sb = torch.empty(Bl, Hl, max(info.max_select, 1), dtype=torch.int32, device=lay["q"].device)
+    scnt = torch.empty(Bl, Hl, dtype=torch.int32, device=lay["q"].device)
+    da.select(l, lay["q"], sb, scnt)  # absp_select materialises every exact score (estimate_scores)
+    torch.cuda.synchronize()
     if not np.array_equal(bits(da.download_scores(l, b)), bits(sc)):
         fails.append("scores")
+    sel_sel = sb[b].cpu().numpy().view(np.uint32)
+    sel_cnt = scnt[b].cpu().numpy().view(np.uint32)
     want_sel = ref.select(sc, T)
-    got_sel = da.download_selection(l)[b]
+    if not all(np.array_equal(sel_sel[h, :sel_cnt[h]], want_sel[h]) for h in range(Hl)):
+        fails.append("selection (absp_select)")
+    got_sel = lay["step_sel"][b]  # the decode step's own selection (fused path), read before
     if not all(np.array_equal(x, y) for x, y in zip(got_sel, want_sel)):
-        fails.append("selection")
+        fails.append("selection (decode step)")
     want_out = ref.decode_gqa(qb, G, T)
     got_out = lay["out"][b].cpu().numpy()
     err = np.abs(got_out.astype(np.float64) - want_out)
@@ -498,6 +509,8 @@ def run_absp(args, w, rank, world, local):
                 for l in range(L):
                     da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
             stream.synchronize()
+            for l in range(L):
+                layers[l]["step_sel"] = da.download_selection(l)
             fails, errs, checked = [], [], []
             # one sequence per rotated layer, up to ~1M verified tokens (cfg2: all 32 layers)
             for l in range(min(L, max(1, (1 << 20) // n))):

@@ -163,7 +163,7 @@ struct AttendWork {
     const uint32_t* chunk_base;  // [units + 1] first chunk of each unit
     const uint32_t* unit_run;    // [units] first CTA of the unit | number of CTA runs << 16
     uint32_t n_work;             // total chunks
-    uint32_t max_runs;           // partial slots per unit = max_runs * kAttnSplits
+    uint32_t max_runs;           // partial slots per unit (one per CTA run)
     uint32_t* unit_done;         // [units] completion counters (zero between launches)
     uint32_t grid;               // persistent CTAs: min(n_work, SMs); CTA c owns chunks
                                  // [c * n_work / grid, (c + 1) * n_work / grid)

@@ -80,7 +80,7 @@ struct WorkList {
     DevBuf<uint32_t> chunk_unit, chunk_idx, chunk_base, unit_done, unit_run;
     DevBuf<uint32_t> page;    // resolved page list, [n_work][ns] (see PageList)
     DevBuf<uint16_t> valid;
-    DevBuf<float> part_o, part_ml;  // one partial slot per (unit, CTA run, consumer warp)
+    DevBuf<float> part_o, part_ml;  // one partial slot per (unit, CTA run): o [8][D], (m, l) [8]
     uint32_t n_work = 0, max_runs = 0, ns = 0, grid = 0;
     uint64_t layout = ~0ull;              // layout version the list was built for
     std::vector<uint32_t> h_base, h_run;  // host copies: an unchanged list is not re-uploaded
@@ -401,8 +401,8 @@ absp_status build_work(Layer& l, uint32_t D, uint32_t P, bool decode, uint32_t c
     ABSP_CUDA(st.zero(wl.unit_done.p, units * 4));
     wl.h_base = base;
     wl.h_run = run;
-    ABSP_CUDA(wl.part_o.ensure(units * runs_res * kAttnSplits * 8 * D));
-    ABSP_CUDA(wl.part_ml.ensure(units * runs_res * kAttnSplits * 16));
+    ABSP_CUDA(wl.part_o.ensure(units * runs_res * 8 * D));
+    ABSP_CUDA(wl.part_ml.ensure(units * runs_res * 16));
     return ABSP_OK;
 }
 

@@ -28,11 +28,14 @@
 //              ~16 mantissa bits), O^T += V^T P^T (M = 16 channels x d/16 tiles,
 //              N = 8 heads, K = the warp's 16 rows). A warp takes its fragments
 //              into registers and releases the stage before the softmax/PV math, so
-//              a stage is held only for QK + ldmatrix. No cross-warp barrier: at the
-//              end of a run of chunks of one unit each warp writes its own partial
-//              (m, l, o[G][d]) and counts its chunks; the warp completing a unit
-//              queues its LSE merge, done by the CTA's warps after the chunk loop
-//              (one warp per (unit, head), loads issued in bulk).
+//              a stage is held only for QK + ldmatrix. At the end of a run of chunks
+//              of one unit (a unit boundary in the CTA's range, or the range's end)
+//              the 8 warps combine their online-softmax states in shared memory (max
+//              rescale, then each thread sums the 8 warps' o values of its columns)
+//              into ONE partial (m, l, o[G][d]) per (unit, CTA run), written to global
+//              memory; the CTA completing a unit (acq_rel counter) queues its LSE merge
+//              over the unit's R runs (R <= 16: one L2 round trip), done after the
+//              chunk loop (one warp per (unit, head)).
 //
 // Bank conflicts without TMA swizzle: a page lands contiguously in smem, so rows
 // of one page are 256 B apart (same banks). Page slots are staggered by 16 B and
@@ -131,8 +134,11 @@ struct SmemHead {  // fixed-size part after the stage tiles
     unsigned long long empty[kStages];
     StageMeta meta[kStages];
     uint32_t npend;          // units this CTA completed (merged after the chunk loop)
+    uint32_t merge_now;      // a completed unit that did not fit the queue
     uint32_t pend[kMaxPend];
     uint16_t p[kWarps][2][8 * kPStride];  // per-warp P tile: bf16 hi + bf16 residual
+    float2 cm[kWarps][8];    // run combine: per-warp (m, l) per head
+    // then (dynamic): float red[kWarps][HP][D], the run combine's o staging, HP heads a pass
 };
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t D, uint32_t P) {
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                                                       const uint32_t* __restrict__ chunk_idx,
                                                       const uint32_t* __restrict__ chunk_base,
                                                       const uint32_t* __restrict__ unit_run,
-                                                      uint32_t n_work, uint32_t max_runs,
+                                                      uint32_t n_work, uint32_t max_runs, uint32_t hp,
                                                       float* __restrict__ part_o,
                                                       float* __restrict__ part_ml,
                                                       uint32_t* __restrict__ unit_done,
@@ -163,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     const uint32_t TB = tile_bytes(D, P);
     const uint32_t slot_stride = P * D * 2 + 16;
     SmemHead<D>& sh = *reinterpret_cast<SmemHead<D>*>(smem + kStages * 2 * TB);
+    float* red = reinterpret_cast<float*>(smem + kStages * 2 * TB + ((sizeof(SmemHead<D>) + 15) & ~size_t(15)));
     const uint32_t smem_base = smem_u32(smem);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -308,34 +315,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     float o[MT][4];
     uint32_t qb[D / 16][2];
 
-    // Partial slot of (unit, run, warp). A run is the part of a unit's chunks one CTA
-    // processes (CTA ranges are contiguous, so run r of unit u belongs to CTA
-    // first_cta(u) + r); every warp of that CTA writes exactly one partial per run.
-    auto slot_of = [&](uint32_t unit, uint32_t run, uint32_t wp) -> size_t {
-        return (size_t(unit) * max_runs + run) * kWarps + wp;
-    };
+    // Partial slot of (unit, run): a run is the part of a unit's chunks one CTA processes
+    // (CTA ranges are contiguous, so run r of unit u belongs to CTA first_cta(u) + r).
+    // part_o [slot][8][D] (heads < G used), part_ml [slot][8] x (m, l).
+    auto slot_of = [&](uint32_t unit, uint32_t run) -> size_t { return size_t(unit) * max_runs + run; };
 
-    // LSE merge of every partial of unit mu for query head h into `out` (one warp).
-    // Every slot of the unit's runs is written each step, so the o rows are loaded
-    // without waiting for (m, l): lanes own D/32 contiguous channels, windows of 32
-    // slots, o loads 8 slots at a time, all independent — about one L2 round trip.
+    // LSE merge of the R run partials of unit mu for query head h into `out` (one warp).
+    // Every slot of the unit's runs is written each step; with R <= 16 all loads are
+    // issued before any is used (one L2 round trip). Lanes own D/32 contiguous channels.
     auto merge = [&](uint32_t mu, uint32_t h) {
         constexpr int PER = D / 32;
-        const uint32_t nslots = (unit_run[mu] >> 16) * kWarps;
-        const float* mlu = part_ml + slot_of(mu, 0, 0) * 16 + h * 2;
-        const float* pou = part_o + (slot_of(mu, 0, 0) * 8 + h) * D + lane * PER;
+        const uint32_t R = unit_run[mu] >> 16;
+        const float* mlu = part_ml + slot_of(mu, 0) * 16 + h * 2;
+        const float* pou = part_o + (slot_of(mu, 0) * 8 + h) * D + lane * PER;
         float acc[PER];
 #pragma unroll
         for (int i = 0; i < PER; ++i) acc[i] = 0.0f;
         float lpart = 0.0f, M = -INFINITY;
-        if (nslots <= 16u) {
-            // the common case (<= 2 CTA runs): every load issued before any is used,
-            // one L2 round trip for the whole merge
+        for (uint32_t base = 0; base < R; base += 16) {
+            const uint32_t n = min(16u, R - base);
             float v[16][PER];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const float* src = pou + size_t(j) * 8 * D;
-                if (uint32_t(j) < nslots) {
+                const float* src = pou + size_t(base + j) * 8 * D;
+                if (uint32_t(j) < n) {
                     if (PER == 4) {
                         const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
                         v[j][0] = t.x; v[j][1] = t.y; v[j][2 % PER] = t.z; v[j][3 % PER] = t.w;
@@ -348,23 +351,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                     for (int i = 0; i < PER; ++i) v[j][i] = 0.0f;
                 }
             }
-            const float mv = lane < nslots ? __ldcg(mlu + lane * 16) : -INFINITY;
-            const float lv = lane < nslots ? __ldcg(mlu + lane * 16 + 1) : 0.0f;
-            float Mw = mv;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) Mw = fmaxf(Mw, __shfl_xor_sync(0xffffffffu, Mw, off));
-            M = Mw;
-            const float wl = (mv == -INFINITY || M == -INFINITY) ? 0.0f : exp2f(mv - M);
-            lpart = wl * lv;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const float wj = __shfl_sync(0xffffffffu, wl, j);
-#pragma unroll
-                for (int i = 0; i < PER; ++i) acc[i] += wj * v[j][i];
-            }
-        }
-        for (uint32_t base = 0; base < nslots && nslots > 16u; base += 32) {
-            const uint32_t n = min(32u, nslots - base);
             const float mv = lane < n ? __ldcg(mlu + (base + lane) * 16) : -INFINITY;
             const float lv = lane < n ? __ldcg(mlu + (base + lane) * 16 + 1) : 0.0f;
             float Mw = mv;
@@ -379,30 +365,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             M = Mn;
             const float wl = mv == -INFINITY ? 0.0f : exp2f(mv - M);  // weight of slot base + lane
             lpart += wl * lv;
-            for (uint32_t s0 = 0; s0 < n; s0 += 8) {
-                float v[8][PER];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float* src = pou + size_t(base + s0 + j) * 8 * D;
-                    if (s0 + j < n) {
-                        if (PER == 4) {
-                            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
-                            v[j][0] = t.x; v[j][1] = t.y; v[j][2 % PER] = t.z; v[j][3 % PER] = t.w;
-                        } else {
-                            const float2 t = __ldcg(reinterpret_cast<const float2*>(src));
-                            v[j][0] = t.x; v[j][1 % PER] = t.y;
-                        }
-                    } else {
+            for (int j = 0; j < 16; ++j) {
+                const float wj = __shfl_sync(0xffffffffu, wl, j);
 #pragma unroll
-                        for (int i = 0; i < PER; ++i) v[j][i] = 0.0f;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float wj = __shfl_sync(0xffffffffu, wl, (s0 + j) & 31);
-#pragma unroll
-                    for (int i = 0; i < PER; ++i) acc[i] += wj * v[j][i];
-                }
+                for (int i = 0; i < PER; ++i) acc[i] += wj * v[j][i];
             }
         }
 #pragma unroll
@@ -417,53 +384,91 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
         if (ready && h == 0 && lane == 0) ready[mu] = 0u;  // every producer is past mu: re-arm
     };
 
-    // Emit this warp's partial of (cur_u, chunks seg_first..seg_last) and count its
-    // chunks; no barrier with the other warps. The warp completing a unit queues its
-    // merge, done by the CTA's warps after the chunk loop.
+    // End of a run: the 8 warps combine their states into the run's single partial
+    // (shared memory, consumer barriers only), the CTA counts the run, and the CTA
+    // completing the unit queues its merge for after the chunk loop.
     auto flush = [&]() {
         float lsum[2] = {l_run[0], l_run[1]};
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc)
 #pragma unroll
             for (int off = 4; off < 32; off <<= 1) lsum[hc] += __shfl_xor_sync(0xffffffffu, lsum[hc], off);
-        const size_t slot = slot_of(cur_u, blockIdx.x - (unit_run[cur_u] & 0xffffu), warp);
+        if (g == 0) {
+            sh.cm[warp][2 * t4] = make_float2(m_run[0], lsum[0]);
+            sh.cm[warp][2 * t4 + 1] = make_float2(m_run[1], lsum[1]);
+        }
+        consumer_sync();
+        // every warp rescales its o to the run maximum M of each of its heads
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            const uint32_t h = 2 * t4 + hc;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sh.cm[w][h].x);
+            const float sc = (m_run[hc] == -INFINITY || M == -INFINITY) ? 0.0f : exp2f(m_run[hc] - M);
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                o[m][hc] *= sc;
+                o[m][2 + hc] *= sc;
+            }
+        }
+        const size_t slot = slot_of(cur_u, blockIdx.x - (unit_run[cur_u] & 0xffffu));
+        if (tid < G) {  // the run's (M, L) per head
+            float M = -INFINITY, Lr = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sh.cm[w][tid].x);
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const float2 c = sh.cm[w][tid];
+                if (c.x != -INFINITY) Lr += c.y * exp2f(c.x - M);
+            }
+            part_ml[slot * 16 + tid * 2] = M;
+            part_ml[slot * 16 + tid * 2 + 1] = Lr;
+        }
+        // o: HP heads per pass through red[warp][HP][D]; each thread then sums the 8 warps
+        // of its columns and stores them
         float* po = part_o + slot * 8 * D;
-        float* ml = part_ml + slot * 16;
+        for (uint32_t h0 = 0; h0 < G; h0 += hp) {
 #pragma unroll
-        for (int m = 0; m < MT; ++m) {
-            const uint32_t c0 = m * 16 + g;
+            for (int m = 0; m < MT; ++m) {
+                const uint32_t c0 = m * 16 + g;
 #pragma unroll
-            for (int hc = 0; hc < 2; ++hc) {
-                const uint32_t h = 2 * t4 + hc;
-                if (h < G) {
-                    po[h * D + c0] = o[m][hc];
-                    po[h * D + c0 + 8] = o[m][2 + hc];
+                for (int hc = 0; hc < 2; ++hc) {
+                    const uint32_t h = 2 * t4 + hc;
+                    if (h >= h0 && h < h0 + hp && h < G) {
+                        float* dst = red + ((warp * hp) + (h - h0)) * D;
+                        dst[c0] = o[m][hc];
+                        dst[c0 + 8] = o[m][2 + hc];
+                    }
                 }
             }
-        }
-        if (g == 0) {  // m and l are warp-uniform per head
-            ml[(2 * t4) * 2] = m_run[0];
-            ml[(2 * t4) * 2 + 1] = lsum[0];
-            ml[(2 * t4 + 1) * 2] = m_run[1];
-            ml[(2 * t4 + 1) * 2 + 1] = lsum[1];
-        }
-        // completion counting: the release publishes this warp's partials to the warp
-        // that completes the unit, whose acquire makes every partial visible to it
-        __syncwarp();
-        uint32_t merge_now = 0;
-        if (lane == 0) {
-            const uint32_t nch = chunk_base[cur_u + 1] - chunk_base[cur_u];
-            const uint32_t mine = seg_last - seg_first + 1;
-            const uint32_t done = atom_add_acq_rel(unit_done + cur_u, mine) + mine;
-            if (done == kWarps * nch) {
-                unit_done[cur_u] = 0u;  // re-arm for the next step
-                const uint32_t slot_p = atomicAdd(&sh.npend, 1u);
-                if (slot_p < uint32_t(kMaxPend)) sh.pend[slot_p] = cur_u;
-                else merge_now = 1u;  // queue full: this warp merges right away
+            consumer_sync();
+            const uint32_t nh = min(hp, G - h0);
+            for (uint32_t e = tid; e < nh * D; e += kConsumers) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) acc += red[(w * hp) * D + e];
+                po[size_t(h0) * D + e] = acc;  // [h][d] rows of heads h0.. are contiguous
             }
+            consumer_sync();
         }
-        if (__shfl_sync(0xffffffffu, merge_now, 0))
-            for (uint32_t h = 0; h < G; ++h) merge(cur_u, h);
+        // run completion: the barrier orders every thread's partial stores before the
+        // release; the acquire of the completing CTA makes all runs' partials visible
+        if (tid == 0) {
+            uint32_t now = 0xffffffffu;
+            const uint32_t runs = unit_run[cur_u] >> 16;
+            const uint32_t done = atom_add_acq_rel(unit_done + cur_u, 1u) + 1u;
+            if (done == runs) {
+                unit_done[cur_u] = 0u;  // re-arm for the next step
+                if (sh.npend < uint32_t(kMaxPend)) sh.pend[sh.npend++] = cur_u;
+                else now = cur_u;  // queue full: merged right away
+            }
+            sh.merge_now = now;
+        }
+        consumer_sync();
+        const uint32_t now = sh.merge_now;
+        if (now != 0xffffffffu)
+            for (uint32_t h = warp; h < G; h += kWarps) merge(now, h);
     };
 
     uint32_t stage = 0, phase = 0, nflush = 0;
@@ -610,31 +615,40 @@ cudaError_t debug_attn_trace(void* dst, size_t bytes) {
 }
 #endif
 
-size_t attend_smem_bytes(uint32_t D, uint32_t P) {
-    return size_t(kStages) * 2 * tile_bytes(D, P) + (D == 64 ? sizeof(SmemHead<64>) : sizeof(SmemHead<128>));
+// Shared memory of one CTA: the stage tiles, the fixed head, and the run combine's
+// staging for hp heads at a time (hp <= G, as many as fit in 227 KB).
+static size_t attend_smem(uint32_t D, uint32_t P, uint32_t hp) {
+    const size_t head = D == 64 ? sizeof(SmemHead<64>) : sizeof(SmemHead<128>);
+    return size_t(kStages) * 2 * tile_bytes(D, P) + ((head + 15) & ~size_t(15)) + size_t(kWarps) * hp * D * 4;
+}
+static uint32_t attend_hp(uint32_t D, uint32_t P, uint32_t G) {
+    uint32_t hp = G < 4 ? G : 4;
+    while (hp > 1 && attend_smem(D, P, hp) > 227 * 1024) --hp;
+    return hp;
 }
 
+size_t attend_smem_bytes(uint32_t D, uint32_t P) { return attend_smem(D, P, attend_hp(D, P, 8)); }
+
 cudaError_t init_attend_attributes() {
-    // the largest footprint over supported (D, P): P = 1 has the most page slots
-    cudaError_t e = cudaFuncSetAttribute(k_attn<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(attend_smem_bytes(64, 1)));
+    cudaError_t e = cudaFuncSetAttribute(k_attn<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_attn<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(attend_smem_bytes(128, 1)));
+    return cudaFuncSetAttribute(k_attn<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages, uint32_t* ready,
                           const AttendWork& wk, float* part_o, float* part_ml, float* out, cudaStream_t s,
                           int* launches) {
-    const size_t smem = attend_smem_bytes(L.D, L.P);
+    const uint32_t hp = attend_hp(L.D, L.P, L.G);
+    const size_t smem = attend_smem(L.D, L.P, hp);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const uint32_t grid = wk.grid;  // = min(n_work, SMs): the CTA runs in unit_run assume it
     if (grid == 0) return cudaSuccess;
     if (L.D == 64)
         launch_pdl(k_attn<64>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, ready, wk.chunk_unit, wk.chunk_idx,
-                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, part_o, part_ml, wk.unit_done, out);
+                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, hp, part_o, part_ml, wk.unit_done, out);
     else
         launch_pdl(k_attn<128>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, ready, wk.chunk_unit, wk.chunk_idx,
-                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, part_o, part_ml, wk.unit_done, out);
+                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, hp, part_o, part_ml, wk.unit_done, out);
     ++*launches;
     return cudaGetLastError();
 }
