@@ -1255,11 +1255,11 @@ namespace absp {
 cudaError_t debug_attn_trace(void* dst, size_t bytes);
 cudaError_t debug_score_trace(void* dst, size_t bytes);
 cudaError_t debug_topk_trace(void* dst, size_t bytes);
-cudaError_t debug_refine_trace(void* dst, size_t bytes, void* cand, size_t cbytes);
+cudaError_t debug_select_trace(void* dst, size_t bytes);
 }
-extern "C" absp_status absp_debug_refine_trace(void* dst, size_t bytes, void* cand, size_t cbytes) {
-    cudaError_t e = absp::debug_refine_trace(dst, bytes, cand, cbytes);
-    return e == cudaSuccess ? ABSP_OK : cuda_fail(e, "debug_refine_trace");
+extern "C" absp_status absp_debug_select_trace(void* dst, size_t bytes) {
+    cudaError_t e = absp::debug_select_trace(dst, bytes);
+    return e == cudaSuccess ? ABSP_OK : cuda_fail(e, "debug_select_trace");
 }
 extern "C" absp_status absp_debug_topk_trace(void* dst, size_t bytes) {
     cudaError_t e = absp::debug_topk_trace(dst, bytes);

@@ -7,7 +7,9 @@
 //   stream  : the producer warp bulk-copies (TMA) the CTA's slice of the unit's packed
 //             code rows into a 4-stage ring, plus q and the unit's scale / zero point.
 //   filter  : consumers compute, per centroid, the exact integer
-//                 I_i = sum_c (256 h_c + l_c) code_ic            (IDP4A, codes 0..15)
+//                 I_i = sum_c (256 h_c + l_c) code_ic   (codes 0..15, integer tensor cores:
+//                 mma.sync m16n8k32 u8 x s8 -> s32 on code words fed by ldmatrix, even
+//                 nibbles as bytes and odd nibbles x16 against separate B columns)
 //             with w_c = fl(q_c s_c) ~ (sigma / 256)(256 h_c + l_c), h, l int8, so
 //             A_i = (sigma / 256) I_i is the score up to the constant C = sum_c q_c zp_c
 //             and a proven per-unit error bound
@@ -50,13 +52,28 @@ constexpr int kSStages = 4;
 constexpr uint32_t kCandCapMax = 2048;   // candidate capacity bound (>= K, K <= T / min B <= 2048)
 constexpr int kBins = 1024;
 
+// Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
+// globaltimer stamps at the phase boundaries (tools/select_trace.py).
+#ifdef ABSP_ATTN_TRACE
+constexpr int kSelTraceSlots = 16;
+__device__ unsigned long long g_sel_trace[2048 * kSelTraceSlots];
+#define SEL_TRACE(slot)                                                                           \
+    do {                                                                                          \
+        if (threadIdx.x == 0 && blockIdx.x < 2048) {                                              \
+            unsigned long long t_;                                                                \
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                 \
+            g_sel_trace[blockIdx.x * kSelTraceSlots + (slot)] = t_;                               \
+        }                                                                                         \
+    } while (0)
+#else
+#define SEL_TRACE(slot) do {} while (0)
+#endif
+
 template <int D>
 struct SelCfg {
     static constexpr int W = D / 8;        // int4 words per code row
-    static constexpr int U = W / 4;        // 16-byte groups per row
     static constexpr int ROWB = W * 4;
     static constexpr int STAGEB = kSRows * ROWB;
-    static constexpr int RING = kSStages * STAGEB;
     static constexpr int QB = 8 * D * 2;   // q rows (G <= 8)
     static constexpr int PB = 2 * D * 4;   // scales + zero points
     static constexpr int TBL = D * 16 * 4; // exact product table
@@ -67,7 +84,7 @@ struct SelCfg {
 //   candidate indices, then the leader's ordered selection).
 struct SelHead {
     unsigned long long bars[2 * kSStages + 1];  // full[NS], empty[NS], params
-    __align__(16) uint32_t wts[4 * 16];  // packed int8 weights: [word][HE, HO, LE, LO] (W <= 16)
+    int8_t hlw[kSCons / 32][2][128];     // per consumer warp: h and l per channel (D <= 128)
     float red[4][kSWarps];       // block reductions
     uint32_t slot[8];            // per-rank local bounds t_r (written by every CTA of the cluster)
     uint32_t st[16];             // misc scalars
@@ -290,13 +307,28 @@ struct SelLayout {
     }
 };
 
+// Integer MMA: C[16x8] (s32) += A[16x32] (u8, row) * B[32x8] (s8, col), exact.
+__device__ __forceinline__ void imma(int* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                     uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
 template <int D>
 __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint16_t* __restrict__ q, uint32_t stages,
                                                        uint32_t slice_cap, uint32_t cand_cap, uint32_t* blocks,
                                                        uint32_t stride, uint32_t* counts, PageList pages,
                                                        uint32_t* ready, float* diag_approx, float* diag_err) {
     using C = SelCfg<D>;
-    constexpr int W = C::W, U = C::U;
+    constexpr int W = C::W, NG = D / 32;  // code words per row, 16-byte groups (32 channels) per row
     extern __shared__ __align__(1024) unsigned char smem[];
     const SelLayout<D> lay(stages, slice_cap, cand_cap);
     unsigned char* ring = smem;
@@ -307,6 +339,8 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     const uint16_t* qrows = reinterpret_cast<const uint16_t*>(prm_raw);
     const float* scl = reinterpret_cast<const float*>(prm_raw + C::QB);
     const float* zps = scl + D;
+    unsigned long long* cand = reinterpret_cast<unsigned long long*>(smem + lay.cand);
+    uint32_t* list = reinterpret_cast<uint32_t*>(smem + lay.list);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t Cn = cluster_size(), r = cluster_rank();
@@ -319,11 +353,13 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     const uint32_t ns = s1 - s0;
     const uint32_t n_chunks = (ns + kSRows - 1) / kSRows;
     const bool resident = n_chunks <= stages;  // the whole slice stays in the ring
+    const bool trailing = !all;                // block N-1 is forced in (scored by the leader)
 
+    SEL_TRACE(0);
     if (tid == 0) {
-        sh.cand = reinterpret_cast<unsigned long long*>(smem + lay.cand);
-        sh.list = reinterpret_cast<uint32_t*>(smem + lay.list);
-        sh.outs = sh.list;  // the candidate list is dead once the composites are in
+        sh.cand = cand;
+        sh.list = list;
+        sh.outs = list;  // the candidate list is dead once the composites are in
         sh.cap = cand_cap;
         for (int i = 0; i < kSStages; ++i) {
             mbar_init(smem_u32(&sh.bars[i]), 1);
@@ -334,7 +370,10 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         sh.local_cnt = 0u;
         sh.cand_cnt = 0u;
         sh.overflow = 0u;
+        sh.nsel = 0u;
+        sh.st[1] = 0u;
     }
+    for (uint32_t i = tid; i < uint32_t(kBins); i += kSThreads) sh.hist[i] = 0u;
     {   // the page resolution at the end reads the sequence's page-table row: warm L2
         const uint32_t row_pages = (du.n_tokens + L.P - 1) / L.P;
         const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
@@ -346,7 +385,13 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     // The attention kernel may be scheduled now: every CTA of this grid is past its wait,
     // i.e. the previous step's attention has completed (its merges re-armed the ready flags).
     griddep_launch_dependents();
+    // the leader's last thread fetches the trailing block's code row now; it is scored
+    // exactly once the product table exists (after barrier #1)
+    uint32_t trail[W];
+    if (r == 0 && trailing && tid == kSThreads - 1) load_row_global<W>(L.codes, du.seg + N - 1, N - 1, trail);
+    SEL_TRACE(1);
     cluster_sync();  // every CTA's shared memory is initialised before any DSMEM access
+    SEL_TRACE(2);
 
     if (warp == kSWarps - 1) {
         // =============================== producer ===============================
@@ -370,160 +415,202 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     } else {
         // =============================== consumers ==============================
         mbar_wait(smem_u32(&sh.bars[2 * kSStages]), 0);
-        // exact product table (score.cu) and the group-summed query
-        for (uint32_t e = tid; e < uint32_t(D * 16); e += kSCons) {
-            const uint32_t c = e >> 4, code = e & 15u;
+        SEL_TRACE(3);
+        const bool asym = L.mode == ABSP_QUANT_ASYM;
+        // Every warp derives the weights itself (identical arithmetic, no CTA barrier):
+        // lane owns channels lane + 32 j. q_c = left-to-right fp32 group sum (score.cu).
+        constexpr int CPL = D / 32;
+        float wv[CPL];
+        float wmax = 0.0f, M = 0.0f;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            const uint32_t c = lane + 32 * j;
             float qc = bf16f(qrows[c]);
-            for (uint32_t g = 1; g < L.G; ++g) qc = __fadd_rn(qc, bf16f(qrows[g * D + c]));
-            const float deq = L.mode == ABSP_QUANT_ASYM ? __fadd_rn(zps[c], __fmul_rn(float(code), scl[c]))
-                                                        : __fmul_rn(float(int(code) - 7), scl[c]);
-            tbl[e] = __fmul_rn(qc, deq);
+            for (uint32_t gq = 1; gq < L.G; ++gq) qc = __fadd_rn(qc, bf16f(qrows[gq * D + c]));
+            wv[j] = __fmul_rn(qc, scl[c]);
+            wmax = fmaxf(wmax, fabsf(wv[j]));
+            float pm = 0.0f;  // max_code |p_c(code)|, the exact products' magnitude
+#pragma unroll
+            for (int code = 0; code < 16; ++code) {
+                const float deq = asym ? __fadd_rn(zps[c], __fmul_rn(float(code), scl[c]))
+                                       : __fmul_rn(float(code - 7), scl[c]);
+                pm = fmaxf(pm, fabsf(__fmul_rn(qc, deq)));
+            }
+            M += pm;
         }
-        // weights w_c = fl(q_c s_c) -> sigma (h + l / 256)
-        float w = 0.0f, qc = 0.0f;
-        if (tid < uint32_t(D)) {
-            qc = bf16f(qrows[tid]);
-            for (uint32_t g = 1; g < L.G; ++g) qc = __fadd_rn(qc, bf16f(qrows[g * D + tid]));
-            w = __fmul_rn(qc, scl[tid]);
-        }
-        float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(w))));
-        if (lane == 0) sh.red[0][warp] = wmax;
-        cons_sync();
-        wmax = 0.0f;
-        for (int i = 0; i < kSCons / 32; ++i) wmax = fmaxf(wmax, sh.red[0][i]);
+        wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(wmax)));
         const float sigma = wmax / 127.0f;
-        float resid = 0.0f, pmax = 0.0f;
-        int h = 0, l = 0;
-        if (tid < uint32_t(D)) {
+        float resid = 0.0f;
+        auto& hlw = sh.hlw;  // this warp's h and l per channel
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            const uint32_t c = lane + 32 * j;
+            int h = 0, l = 0;
             if (sigma > 0.0f) {
-                h = __float2int_rn(w / sigma);
+                h = __float2int_rn(wv[j] / sigma);
                 h = h > 127 ? 127 : (h < -127 ? -127 : h);
-                l = __float2int_rn((w - float(h) * sigma) * 256.0f / sigma);
+                l = __float2int_rn((wv[j] - float(h) * sigma) * 256.0f / sigma);
                 l = l > 127 ? 127 : (l < -127 ? -127 : l);
             }
-            resid = fabsf(w - sigma * (float(h) + float(l) * 0.00390625f)) + fabsf(w) * 0x1p-23f;
-            for (int code = 0; code < 16; ++code) pmax = fmaxf(pmax, fabsf(tbl[tid * 16 + code]));
-        }
-        // packed weights: word j, byte b <- channel 8j + 2b (even) / 8j + 2b + 1 (odd)
-        if (tid < uint32_t(D)) {
-            const uint32_t j = tid >> 3, k = tid & 7u, b = k >> 1, odd = k & 1u;
-            unsigned char* wb = reinterpret_cast<unsigned char*>(sh.wts);
-            wb[(j * 4 + odd) * 4 + b] = uint8_t(int8_t(h));
-            wb[(j * 4 + 2 + odd) * 4 + b] = uint8_t(int8_t(l));
+            hlw[warp][0][c] = int8_t(h);
+            hlw[warp][1][c] = int8_t(l);
+            resid += fabsf(wv[j] - sigma * (float(h) + float(l) * 0.00390625f)) + fabsf(wv[j]) * 0x1p-23f;
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             resid += __shfl_xor_sync(0xffffffffu, resid, off);
-            pmax += __shfl_xor_sync(0xffffffffu, pmax, off);
+            M += __shfl_xor_sync(0xffffffffu, M, off);
         }
-        if (lane == 0) {
-            sh.red[1][warp] = resid;
-            sh.red[2][warp] = pmax;
-        }
-        cons_sync();
-        float R = 0.0f, M = 0.0f;
-        for (int i = 0; i < kSCons / 32; ++i) {
-            R += sh.red[1][i];
-            M += sh.red[2][i];
-        }
-        const float E = M * 0x1p-14f + 15.0f * R * 1.01f;
+        const float E = M * 0x1p-14f + 15.0f * resid * 1.01f;
         const uint32_t e_int = sigma > 0.0f ? uint32_t(fminf(ceilf(E * 256.0f / sigma), 1.0e9f)) + 2u : 0xffffffffu;
         if (tid == 0) {
             sh.st[0] = e_int;
             if (diag_err && r == 0) diag_err[u] = E;
         }
-        const uint4* wq = reinterpret_cast<const uint4*>(sh.wts);  // [word] {HE, HO, LE, LO}, broadcast loads
+        __syncwarp();
+        // B fragments (column n = lane / 4 of the m16n8k32 tile), group G, word j = 4G + t4:
+        //   col 0: h of the even channels 8j + 0,2,4,6   col 1: l of them
+        //   col 2: h of the odd channels (their codes arrive x16, so col 2 sums 16 x h . code)
+        //   col 3: l of the odd channels                  cols 4-7: zero
+        const uint32_t gq = lane >> 2, t4 = lane & 3;
+        uint32_t bfr[NG][2];
+#pragma unroll
+        for (int G = 0; G < NG; ++G) {
+            const uint32_t j = 4 * G + t4;
+            uint32_t v = 0;
+            if (gq < 4) {
+                const int8_t* src = hlw[warp][gq & 1];
+                const uint32_t odd = gq >> 1;
+#pragma unroll
+                for (int bb = 0; bb < 4; ++bb) v |= uint32_t(uint8_t(src[8 * j + 2 * bb + odd])) << (8 * bb);
+            }
+            bfr[G][0] = gq < 2 ? v : 0u;
+            bfr[G][1] = (gq >= 2 && gq < 4) ? v : 0u;
+        }
+        // exact product table (for the refine): this warp's 16 channels x 16 codes
+        {
+            const uint32_t c = warp * (D / 8) + (lane % (D / 8)), code0 = (lane / (D / 8)) * (16 * D / 8 / 32);
+            float qc = bf16f(qrows[c]);
+            for (uint32_t g2 = 1; g2 < L.G; ++g2) qc = __fadd_rn(qc, bf16f(qrows[g2 * D + c]));
+#pragma unroll
+            for (uint32_t k = 0; k < 16 * D / 8 / 32; ++k) {
+                const uint32_t code = code0 + k;
+                const float deq = asym ? __fadd_rn(zps[c], __fmul_rn(float(code), scl[c]))
+                                       : __fmul_rn(float(int(code) - 7), scl[c]);
+                tbl[c * 16 + code] = __fmul_rn(qc, deq);
+            }
+        }
+        SEL_TRACE(4);
 
-        // ---- filter: integer scores of the slice -> keys (order-preserving u32) ----
+        // ---- filter: exact integer scores I_i of the slice on the tensor cores ----
         uint32_t kmin = 0xffffffffu, kmax = 0u;
+        const float a_scale = sigma * 0.00390625f;
         for (uint32_t c = 0; c < n_chunks; ++c) {
             const uint32_t stg = c % stages;
             mbar_wait(smem_u32(&sh.bars[stg]), (c / stages) & 1);
-            const uint32_t row = c * kSRows + tid;
-            if (row < ns) {
-                const unsigned char* src = ring + size_t(stg) * C::STAGEB + tid * C::ROWB;
-                const uint32_t key = code_row_key(s0 + row, W);
-                int sh_ = 0, sl_ = 0;
+            const uint32_t sbase = smem_u32(ring + size_t(stg) * C::STAGEB);
+            for (uint32_t tile = warp; tile < uint32_t(kSRows / 16); tile += kSCons / 32) {
+                const uint32_t row0 = c * kSRows + tile * 16;  // slice-relative
+                if (row0 >= ns) break;
+                int acc[4] = {0, 0, 0, 0};
+                // ldmatrix.x4: lanes 8m.. address matrix m: rows (m & 1) * 8 + 0..7, group 2gp + (m >> 1)
+                const uint32_t mi = lane >> 3, rr = (lane & 7) + (mi & 1) * 8;
+                const uint32_t rkey = code_row_key(s0 + row0 + rr, W);
+                const uint32_t raddr = sbase + (tile * 16 + rr) * C::ROWB;
 #pragma unroll
-                for (int g = 0; g < U; ++g) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(src + ((g ^ key) << 4));
-                    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const uint4 wj = wq[4 * g + t];
-                        const int lo = int(wd[t] & 0x0F0F0F0Fu), hi = int((wd[t] >> 4) & 0x0F0F0F0Fu);
-                        sh_ = __dp4a(lo, int(wj.x), sh_);
-                        sh_ = __dp4a(hi, int(wj.y), sh_);
-                        sl_ = __dp4a(lo, int(wj.z), sl_);
-                        sl_ = __dp4a(hi, int(wj.w), sl_);
+                for (int gp = 0; gp < NG / 2; ++gp) {
+                    const uint32_t grp = 2 * gp + (mi >> 1);
+                    uint32_t x0, x1, x2, x3;  // rows g / g+8 of groups 2gp / 2gp+1, word t4
+                    ldsm_x4(raddr + ((grp ^ rkey) << 4), x0, x1, x2, x3);
+                    constexpr uint32_t LO = 0x0F0F0F0Fu, HI = 0xF0F0F0F0u;
+                    imma(acc, x0 & LO, x1 & LO, x0 & HI, x1 & HI, bfr[2 * gp][0], bfr[2 * gp][1]);
+                    imma(acc, x2 & LO, x3 & LO, x2 & HI, x3 & HI, bfr[2 * gp + 1][0], bfr[2 * gp + 1][1]);
+                }
+                // t4 = 0 holds (even h, even l), t4 = 1 (16 x odd h, 16 x odd l), rows g and g+8
+                const int o0 = __shfl_down_sync(0xffffffffu, acc[0], 1), o1 = __shfl_down_sync(0xffffffffu, acc[1], 1);
+                const int o2 = __shfl_down_sync(0xffffffffu, acc[2], 1), o3 = __shfl_down_sync(0xffffffffu, acc[3], 1);
+                if (t4 == 0) {
+                    const int I0 = (acc[0] + (o0 >> 4)) * 256 + acc[1] + (o1 >> 4);
+                    const int I1 = (acc[2] + (o2 >> 4)) * 256 + acc[3] + (o3 >> 4);
+                    const uint32_t ra = row0 + gq, rb = ra + 8;
+                    if (ra < ns) {
+                        const uint32_t k = uint32_t(I0) ^ 0x80000000u;
+                        keys[ra] = k;
+                        kmin = min(kmin, k);
+                        kmax = max(kmax, k);
+                        if (diag_approx) diag_approx[du.seg + s0 + ra] = float(I0) * a_scale;
+                    }
+                    if (rb < ns) {
+                        const uint32_t k = uint32_t(I1) ^ 0x80000000u;
+                        keys[rb] = k;
+                        kmin = min(kmin, k);
+                        kmax = max(kmax, k);
+                        if (diag_approx) diag_approx[du.seg + s0 + rb] = float(I1) * a_scale;
                     }
                 }
-                const int I = sh_ * 256 + sl_;
-                const uint32_t k = uint32_t(I) ^ 0x80000000u;
-                keys[row] = k;
-                kmin = min(kmin, k);
-                kmax = max(kmax, k);
-                if (diag_approx) diag_approx[du.seg + s0 + row] = float(I) * (sigma * 0.00390625f);
             }
             if (!resident) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&sh.bars[kSStages + stg]));
             }
         }
-        kmin = __reduce_min_sync(0xffffffffu, kmin);
-        kmax = __reduce_max_sync(0xffffffffu, kmax);
-        if (lane == 0) {
-            sh.red[0][warp] = __uint_as_float(kmin);
-            sh.red[1][warp] = __uint_as_float(kmax);
-        }
-        for (uint32_t i = tid; i < uint32_t(kBins); i += kSCons) sh.hist[i] = 0u;
-        cons_sync();
-        kmin = 0xffffffffu;
-        kmax = 0u;
-        for (int i = 0; i < kSCons / 32; ++i) {
-            kmin = min(kmin, __float_as_uint(sh.red[0][i]));
-            kmax = max(kmax, __float_as_uint(sh.red[1][i]));
-        }
-        // ---- local lower bound of the k_r-th largest (1024-bin histogram) ----
+        SEL_TRACE(5);
+        // ---- local lower bound t_r of the k_r-th largest: 1024 bins of the key range ----
         uint32_t t_r = 0u;
-        if (!all && K > 1) {
-            const uint32_t kr = (K - 1 + Cn - 1) / Cn;
-            if (ns >= kr) {
-                const uint64_t R64 = uint64_t(kmax - kmin) + 1;
-                for (uint32_t i = tid; i < ns; i += kSCons)
-                    atomicAdd(&sh.hist[uint32_t((uint64_t(keys[i] - kmin) * kBins) / R64)], 1u);
-                cons_sync();
-                if (tid < 32) {  // bin holding the kr-th largest, counted from the top
-                    constexpr int PER = kBins / 32;
-                    uint32_t tot = 0;
-                    for (int j = 0; j < PER; ++j) tot += sh.hist[kBins - 1 - (lane * PER + j)];
-                    uint32_t incl = tot;
+        const uint32_t kr = (K - 1 + Cn - 1) / Cn;
+        if (!all && K > 1 && ns >= kr) {
+            kmin = __reduce_min_sync(0xffffffffu, kmin);
+            kmax = __reduce_max_sync(0xffffffffu, kmax);
+            if (lane == 0) {
+                sh.red[0][warp] = __uint_as_float(kmin);
+                sh.red[1][warp] = __uint_as_float(kmax);
+            }
+            cons_sync();
+            kmin = 0xffffffffu;
+            kmax = 0u;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= uint32_t(o)) incl += v;
-                    }
-                    uint32_t cum = incl - tot;
-                    if (cum < kr && kr <= incl) {
-                        for (int j = 0; j < PER; ++j) {
-                            const uint32_t b = kBins - 1 - (lane * PER + j);
-                            cum += sh.hist[b];
-                            if (cum >= kr) {  // lower edge: the smallest key mapping to bin b
-                                sh.st[1] = kmin + uint32_t((uint64_t(b) * R64 + kBins - 1) / kBins);
-                                break;
-                            }
+            for (int i = 0; i < kSCons / 32; ++i) {
+                kmin = min(kmin, __float_as_uint(sh.red[0][i]));
+                kmax = max(kmax, __float_as_uint(sh.red[1][i]));
+            }
+            const uint32_t span = kmax - kmin;  // bins: (key - kmin) >> shift < 1024
+            const uint32_t shift = span < uint32_t(kBins) ? 0u : 32u - __clz(span) - 10u;
+            for (uint32_t i = tid; i < ns; i += kSCons) atomicAdd(&sh.hist[(keys[i] - kmin) >> shift], 1u);
+            cons_sync();
+            if (warp == 0) {  // bin holding the kr-th largest, counted from the top
+                constexpr int PER = kBins / 32;
+                uint32_t tot = 0;
+#pragma unroll 8
+                for (int j = 0; j < PER; ++j) tot += sh.hist[kBins - 1 - (lane * PER + j)];
+                uint32_t incl = tot;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= uint32_t(o)) incl += v;
+                }
+                uint32_t cum = incl - tot;
+                if (cum < kr && kr <= incl) {
+                    for (int j = 0; j < PER; ++j) {
+                        const uint32_t b = kBins - 1 - (lane * PER + j);
+                        cum += sh.hist[b];
+                        if (cum >= kr) {  // every key of bin b and above is >= its lower edge
+                            sh.st[1] = kmin + (b << shift);
+                            break;
                         }
                     }
                 }
-                cons_sync();
-                t_r = sh.st[1];
             }
+            cons_sync();
+            t_r = sh.st[1];
         }
+        SEL_TRACE(6);
         if (tid < Cn) st_cluster_u32(dsmem(&sh.slot[r], tid), t_r);  // every CTA gets every t_r
     }
-    cluster_sync();  // #1: slices scored, bounds exchanged
+    cluster_sync();  // #1: slices scored, bounds exchanged, product table complete
+    SEL_TRACE(7);
 
     // ---- candidates of this slice, exact scores, composites to the leader ----
+    if (r == 0 && trailing && tid == kSThreads - 1) sh.st[3] = order_key(exact_row<W>(trail, tbl));
     const uint32_t e_int = sh.st[0];
     uint32_t thr = 0u;
     if (!all && K > 1) {
@@ -534,14 +621,14 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     if (warp < kSCons / 32 && (all || K > 1)) {
         for (uint32_t b0 = warp * 32; b0 < ns; b0 += kSCons) {  // warp-uniform trip count
             const uint32_t i = b0 + lane;
-            const bool cand = i < ns && keys[i] >= thr;
-            const uint32_t m = __ballot_sync(0xffffffffu, cand);
+            const bool cnd = i < ns && keys[i] >= thr;
+            const uint32_t m = __ballot_sync(0xffffffffu, cnd);
             uint32_t base = 0;
             if (lane == 0 && m) base = atomicAdd(&sh.local_cnt, __popc(m));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (cand) {
+            if (cnd) {
                 const uint32_t p = base + __popc(m & ((1u << lane) - 1u));
-                if (p < cand_cap) sh.list[p] = i;
+                if (p < cand_cap) list[p] = i;
             }
         }
     }
@@ -558,13 +645,13 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             if (tid == 0) red_or_cluster(leader_of, 1u);
         } else {
             for (uint32_t j = tid; j < nl; j += kSThreads) {
-                const uint32_t i = sh.list[j];
+                const uint32_t i = list[j];
                 uint32_t wd[W];
                 if (resident) {
-                    const unsigned char* src = ring + size_t(i / kSRows) * C::STAGEB + (i % kSRows) * C::ROWB;  // resident: stage i / rows
+                    const unsigned char* src = ring + size_t(i / kSRows) * C::STAGEB + (i % kSRows) * C::ROWB;
                     const uint32_t key = code_row_key(s0 + i, W);
 #pragma unroll
-                    for (int g = 0; g < U; ++g) {
+                    for (int g = 0; g < W / 4; ++g) {
                         const uint4 v = *reinterpret_cast<const uint4*>(src + ((g ^ key) << 4));
                         wd[4 * g] = v.x;
                         wd[4 * g + 1] = v.y;
@@ -576,39 +663,99 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
                 }
                 const float x = exact_row<W>(wd, tbl);
                 const unsigned long long comp = (uint64_t(order_key(x)) << 32) | uint32_t(~(s0 + i));
-                st_cluster_u64(dsmem(&sh.cand[pos0 + j], 0), comp);
+                st_cluster_u64(dsmem(&cand[pos0 + j], 0), comp);
             }
         }
     }
+    SEL_TRACE(8);
     cluster_sync();  // #2: every composite has landed in the leader
+    SEL_TRACE(9);
     if (r != 0) return;
 
     // ================================ leader ===================================
-    unsigned long long ct = 0ull;
-    if (!all) {  // the trailing block's exact score (forced into the selection)
-        if (tid == 0) {
-            uint32_t wd[W];
-            load_row_global<W>(L.codes, du.seg + N - 1, N - 1, wd);
-            const float x = exact_row<W>(wd, tbl);
-            sh.st[3] = order_key(x);
+    const unsigned long long ct = trailing ? (uint64_t(sh.st[3]) << 32) | uint32_t(~(N - 1)) : 0ull;
+    const uint32_t n = sh.cand_cnt;
+    const uint32_t K1 = trailing ? K - 1 : n;
+    SEL_TRACE(10);
+    if (trailing && (K > 1) && (sh.overflow || n < K1)) {  // mass ties: exact fallback
+        exact_fallback<W>(L, du, sh, tbl, K, ct);
+        publish_selection(L, du, u, sh.outs, K, blocks, stride, counts, pages, ready);
+        SEL_TRACE(12);
+        return;
+    }
+    // Order and publish in one pass: the rank of a candidate among the candidates is its
+    // output position (composites are distinct); the trailing block goes after every
+    // winner above it. The thread that ranks a winner writes its block id and resolves
+    // its pages straight into the attention producer's page list.
+    const uint32_t n_sel = trailing ? K : n;
+    const uint32_t ppb = du.block / L.P;
+    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+    const uint32_t head_base = du.head * uint32_t(L.pool_pages);
+    const size_t pbase = pages.page ? size_t(pages.chunk_base[u]) * pages.ns : 0;
+    auto emit = [&](uint32_t p, uint32_t blk) {
+        blocks[size_t(u) * stride + p] = blk;
+        if (!pages.page) return;
+        for (uint32_t pp = 0; pp < ppb; ++pp) {
+            const uint32_t t0 = blk * du.block + pp * L.P;
+            uint32_t v = 0, page = 0;
+            if (t0 < du.n_tokens) {
+                v = min(L.P, du.n_tokens - t0);
+                page = head_base + __ldg(pt + t0 / L.P);
+            }
+            pages.page[pbase + size_t(p) * ppb + pp] = page;
+            pages.valid[pbase + size_t(p) * ppb + pp] = uint16_t(v);
         }
-        __syncthreads();
-        ct = (uint64_t(sh.st[3]) << 32) | uint32_t(~(N - 1));
+    };
+    bool above = false;  // a winner ranked before the trailing block
+    if (trailing && K == 1) {
+        // the trailing block only
+    } else if (n <= uint32_t(kSThreads)) {
+        const uint32_t tpc = n <= 36 ? 8u : n <= 72 ? 4u : n <= 144 ? 2u : 1u;  // threads per candidate
+        const uint32_t j = tid / tpc, part = tid % tpc;
+        const bool valid = j < n;
+        const unsigned long long me = valid ? cand[j] : 0ull;
+        uint32_t rank = 0;
+        if (valid) {
+#pragma unroll 4
+            for (uint32_t o = part; o < n; o += tpc) rank += cand[o] > me;
+        }
+        for (uint32_t off = 1; off < tpc; off <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
+        if (valid && part == 0 && rank < K1) {
+            above = trailing && me > ct;
+            emit(rank + (trailing && ct > me ? 1u : 0u), ~uint32_t(me));
+        }
+    } else {  // large candidate sets (large budgets): sort, then emit by position
+        sort_desc(cand, n);
+        for (uint32_t p = tid; p < K1; p += kSThreads) {
+            const unsigned long long me = cand[p];
+            if (trailing && me > ct) atomicAdd(&sh.nsel, 1u);
+            emit(p + (trailing && ct > me ? 1u : 0u), ~uint32_t(me));
+        }
     }
-    uint32_t n_sel;
-    if (!all && K == 1) {
-        if (tid == 0) sh.outs[0] = N - 1;
-        n_sel = 1;
-    } else if (!all && (sh.overflow || sh.cand_cnt < K - 1)) {
-        exact_fallback<W>(L, du, sh, tbl, K, ct);  // (all: N <= K <= cand_cap never overflows)
-        n_sel = K;
-    } else {
-        n_sel = order_selection(sh, sh.cand_cnt, K, !all, ct, N);
+    SEL_TRACE(11);
+    uint32_t n_above = __syncthreads_count(above);
+    if (n > uint32_t(kSThreads)) n_above = sh.nsel;  // (set before the barrier above)
+    if (trailing && tid == 0) emit(n_above, N - 1);
+    if (pages.page) {  // the rest of the unit's last attention chunk: empty slots
+        const uint32_t E = kAttnChunkRows / du.block;
+        const uint32_t slot_end = ((n_sel + E - 1) / E * E) * ppb;
+        for (uint32_t s = n_sel * ppb + tid; s < slot_end; s += kSThreads) {
+            pages.page[pbase + s] = 0u;
+            pages.valid[pbase + s] = 0u;
+        }
     }
-    publish_selection(L, du, u, sh.outs, n_sel, blocks, stride, counts, pages, ready);
+    if (tid == 0) counts[u] = n_sel;
+    __syncthreads();
+    if (ready && tid == 0)  // release: cumulative over the CTA's writes ordered by the barrier
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(ready + u), "r"(1u) : "memory");
+    SEL_TRACE(12);
 }
 
 }  // namespace
+
+#ifdef ABSP_ATTN_TRACE
+cudaError_t debug_select_trace(void* dst, size_t bytes) { return cudaMemcpyFromSymbol(dst, g_sel_trace, bytes); }
+#endif
 
 bool select_fused_supported(const LayerView& L) {
     return L.bits == 4 && L.method == ABSP_CENTROID_MEAN && (L.D == 64 || L.D == 128) && L.G <= 8;

@@ -14,9 +14,10 @@ from paper_2605_12110_b200 import (BlockAssignment, DecodeAttention, EngineConfi
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg3")
 ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--batch", type=int, default=0, help="sequences (0: the workload's global batch)")
 a = ap.parse_args()
 w = WORKLOADS[a.workload]
-B, n, H, G, d, P, T = w["batch"], w["n"], w["H"], w["G"], w["d"], w["P"], w["T"]
+B, n, H, G, d, P, T = a.batch or w["batch"], w["n"], w["H"], w["G"], w["d"], w["P"], w["T"]
 pages = B * ((n + P - 1) // P)
 cfg = EngineConfig(num_heads=H, head_dim=d, page_size=P, candidate_block_sizes=tuple(w["cands"]), token_budget=T,
                    quant=QuantSpec(4), num_q_heads=H * G, max_batch=B, max_seq_len=n)

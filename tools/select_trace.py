@@ -1,5 +1,7 @@
-"""Decode-step selection timeline (debug): cfg-3 decode steps with lib/libabsp_trace.so;
-per-unit phase stamps of k_select_refine and its candidate counts. Tooling, not product."""
+"""Fused-selection timeline (debug): one decode step of a layer with lib/libabsp_trace.so
+after an L2 flush; per-CTA globaltimer stamps of k_select's phases (select.cu SEL_TRACE)
+and the attention CTAs' first data / end (attend.cu). Tooling, not product.
+usage: python tools/select_trace.py [workload] [batch]"""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -12,13 +14,15 @@ import torch  # noqa: E402
 from paper_2605_12110_b200 import _abi  # noqa: E402
 
 _abi._lib = _abi.load(ROOT / "paper_2605_12110_b200" / "lib" / "libabsp_trace.so")
-_abi._lib.absp_debug_refine_trace.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t]
+for f in ("absp_debug_select_trace", "absp_debug_attn_trace"):
+    getattr(_abi._lib, f).argtypes = [C.c_void_p, C.c_size_t]
 from bench import SEED, WORKLOADS  # noqa: E402
 from paper_2605_12110_b200 import (BlockAssignment, DecodeAttention, EngineConfig, QuantSpec,  # noqa: E402
                                    fill_synthetic_bf16)
 
 w = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg3"]
-B, n, H, G, d, P, T = w["batch"], w["n"], w["H"], w["G"], w["d"], w["P"], w["T"]
+B = int(sys.argv[2]) if len(sys.argv) > 2 else w["batch"]
+n, H, G, d, P, T = w["n"], w["H"], w["G"], w["d"], w["P"], w["T"]
 pages = B * ((n + P - 1) // P)
 cfg = EngineConfig(num_heads=H, head_dim=d, page_size=P, candidate_block_sizes=tuple(w["cands"]), token_budget=T,
                    quant=QuantSpec(4), num_q_heads=H * G, max_batch=B, max_seq_len=n)
@@ -33,17 +37,42 @@ pt = torch.arange(pages, dtype=torch.int32, device="cuda").reshape(B, -1)
 da.bind(0, k, v, pt, [n] * B)
 da.build_store(0)
 out = torch.empty(B, H * G, d, dtype=torch.float32, device="cuda")
-for _ in range(3):
-    da.decode_step(0, q, out)
-torch.cuda.synchronize()
-units = B * H
-tr = np.zeros((1024, 8), np.uint64)
-cand = np.zeros(1024, np.uint32)
-_abi.check(_abi._lib.absp_debug_refine_trace(tr.ctypes.data, tr.nbytes, cand.ctypes.data, cand.nbytes))
-t0 = tr[:units, 0].min()
+stream = torch.cuda.Stream()
+with torch.cuda.stream(stream):
+    for _ in range(3):
+        da.decode_step(0, q, out, stream)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        da.decode_step(0, q, out, stream)
+flush = torch.empty(1 << 28, dtype=torch.int8, device="cuda")
+names = ["start", "wait done", "cluster0", "params", "table+wts", "filter done", "bound", "cluster1",
+         "cands scored", "cluster2", "trailing", "ordered", "published"]
 pct = lambda a: " ".join(f"{x:7.2f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
-print(f"{units} unit CTAs, candidates pctl 0/10/50/90/100: {pct(cand[:units].astype(float))}")
-names = ["start", "after griddep wait", "loads", "kth bound", "candidates+table", "exact scored", "ordered", "end"]
-for j, nm in enumerate(names):
-    rel = (tr[:units, j].astype(np.int64) - int(t0)) / 1e3
-    print(f"  {nm:20s} {pct(rel)}")
+for rep in range(2):
+    flush.fill_(rep)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    st = np.zeros((2048, 16), np.uint64)
+    at = np.zeros((160, 256), np.uint64)
+    _abi.check(_abi._lib.absp_debug_select_trace(st.ctypes.data, st.nbytes))
+    _abi.check(_abi._lib.absp_debug_attn_trace(at.ctypes.data, at.nbytes))
+    ncta = int((st[:, 0] > 0).sum())
+    st = st[:ncta]
+    t0 = st[:, 0].min()
+    print(f"rep {rep}: {ncta} select CTAs (us from the first start; pctl 0/10/50/90/100)")
+    for i, nm in enumerate(names):
+        col = st[:, i]
+        col = col[col > 0]
+        if len(col):
+            print(f"  {nm:14s} {pct((col.astype(np.float64) - t0) / 1e3)}  (n={len(col)})")
+    lead = st[:, 13][st[:, 12] > 0]
+    print("  candidates/unit", pct(lead & 0xffffffff), " overflow units", int(((lead >> 32) > 0).sum()))
+    a0 = at[:, 0]
+    live = a0 > 0
+    if live.any():
+        print(f"  attn CTA start {pct((at[live, 0].astype(np.float64) - t0) / 1e3)}")
+        fd = at[live, 64]
+        print(f"  attn 1st data  {pct((fd[fd > 0].astype(np.float64) - t0) / 1e3)}")
+        ends = at[live][:, 242:250].max(1)
+        print(f"  attn end       {pct((ends.astype(np.float64) - t0) / 1e3)}")
