@@ -85,6 +85,8 @@ struct SelCfg {
 struct SelHead {
     unsigned long long bars[2 * kSStages + 1];  // full[NS], empty[NS], params
     int8_t hlw[kSCons / 32][2][128];     // per consumer warp: h and l per channel (D <= 128)
+    uint32_t tpg[kAttnChunkRows];        // leader: the trailing block's pool pages (prefetched)
+    uint32_t tvl[kAttnChunkRows];        //         and their valid rows
     float red[4][kSWarps];       // block reductions
     uint32_t slot[8];            // per-rank local bounds t_r (written by every CTA of the cluster)
     uint32_t st[16];             // misc scalars
@@ -111,6 +113,12 @@ __device__ __forceinline__ uint32_t cluster_size() {
 }
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 // Address of `p` (this CTA's shared memory) in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t dsmem(const void* p, uint32_t rank) {
@@ -389,8 +397,19 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     // exactly once the product table exists (after barrier #1)
     uint32_t trail[W];
     if (r == 0 && trailing && tid == kSThreads - 1) load_row_global<W>(L.codes, du.seg + N - 1, N - 1, trail);
+    if (r == 0 && trailing && warp == kSWarps - 1 && pages.page) {  // and its pages
+        const uint32_t ppb = du.block / L.P;
+        const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+        for (uint32_t pp = lane; pp < ppb; pp += 32) {
+            const uint32_t t0 = (N - 1) * du.block + pp * L.P;
+            sh.tvl[pp] = t0 < du.n_tokens ? min(L.P, du.n_tokens - t0) : 0u;
+            sh.tpg[pp] = t0 < du.n_tokens ? du.head * uint32_t(L.pool_pages) + __ldg(pt + t0 / L.P) : 0u;
+        }
+    }
     SEL_TRACE(1);
-    cluster_sync();  // every CTA's shared memory is initialised before any DSMEM access
+    // this CTA's shared memory is initialised: no CTA of the cluster touches another's
+    // before the matching wait (just before the first DSMEM access, after the filter)
+    cluster_arrive();
     SEL_TRACE(2);
 
     if (warp == kSWarps - 1) {
@@ -420,36 +439,43 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         // Every warp derives the weights itself (identical arithmetic, no CTA barrier):
         // lane owns channels lane + 32 j. q_c = left-to-right fp32 group sum (score.cu).
         constexpr int CPL = D / 32;
+        const uint32_t G = L.G;
+        auto qsum = [&](uint32_t c) {
+            float qg[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) qg[g] = uint32_t(g) < G ? bf16f(qrows[g * D + c]) : 0.0f;  // independent loads
+            float qc = qg[0];
+#pragma unroll
+            for (int g = 1; g < 8; ++g)
+                if (uint32_t(g) < G) qc = __fadd_rn(qc, qg[g]);
+            return qc;
+        };
         float wv[CPL];
         float wmax = 0.0f, M = 0.0f;
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
             const uint32_t c = lane + 32 * j;
-            float qc = bf16f(qrows[c]);
-            for (uint32_t gq = 1; gq < L.G; ++gq) qc = __fadd_rn(qc, bf16f(qrows[gq * D + c]));
-            wv[j] = __fmul_rn(qc, scl[c]);
+            const float qc = qsum(c), sc = scl[c], zp = zps[c];
+            wv[j] = __fmul_rn(qc, sc);
             wmax = fmaxf(wmax, fabsf(wv[j]));
-            float pm = 0.0f;  // max_code |p_c(code)|, the exact products' magnitude
-#pragma unroll
-            for (int code = 0; code < 16; ++code) {
-                const float deq = asym ? __fadd_rn(zps[c], __fmul_rn(float(code), scl[c]))
-                                       : __fmul_rn(float(code - 7), scl[c]);
-                pm = fmaxf(pm, fabsf(__fmul_rn(qc, deq)));
-            }
-            M += pm;
+            // max_code |p_c(code)|: every rounding step is monotone in the code, so the
+            // magnitude of the exact product peaks at code 0 or code 15
+            const float d0 = asym ? zp : __fmul_rn(-7.0f, sc);
+            const float d15 = asym ? __fadd_rn(zp, __fmul_rn(15.0f, sc)) : __fmul_rn(8.0f, sc);
+            M += fmaxf(fabsf(__fmul_rn(qc, d0)), fabsf(__fmul_rn(qc, d15)));
         }
         wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(wmax)));
-        const float sigma = wmax / 127.0f;
+        const float sigma = wmax / 127.0f, inv = wmax > 0.0f ? 127.0f / wmax : 0.0f;
         float resid = 0.0f;
         auto& hlw = sh.hlw;  // this warp's h and l per channel
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
             const uint32_t c = lane + 32 * j;
             int h = 0, l = 0;
-            if (sigma > 0.0f) {
-                h = __float2int_rn(wv[j] / sigma);
+            if (sigma > 0.0f) {  // any h, l are valid: the bound uses the actual residual
+                h = __float2int_rn(wv[j] * inv);
                 h = h > 127 ? 127 : (h < -127 ? -127 : h);
-                l = __float2int_rn((wv[j] - float(h) * sigma) * 256.0f / sigma);
+                l = __float2int_rn((wv[j] - float(h) * sigma) * 256.0f * inv);
                 l = l > 127 ? 127 : (l < -127 ? -127 : l);
             }
             hlw[warp][0][c] = int8_t(h);
@@ -462,7 +488,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             M += __shfl_xor_sync(0xffffffffu, M, off);
         }
         const float E = M * 0x1p-14f + 15.0f * resid * 1.01f;
-        const uint32_t e_int = sigma > 0.0f ? uint32_t(fminf(ceilf(E * 256.0f / sigma), 1.0e9f)) + 2u : 0xffffffffu;
+        const uint32_t e_int = sigma > 0.0f ? uint32_t(fminf(ceilf(E * 256.0f * inv), 1.0e9f)) + 2u : 0xffffffffu;
         if (tid == 0) {
             sh.st[0] = e_int;
             if (diag_err && r == 0) diag_err[u] = E;
@@ -489,15 +515,14 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         }
         // exact product table (for the refine): this warp's 16 channels x 16 codes
         {
-            const uint32_t c = warp * (D / 8) + (lane % (D / 8)), code0 = (lane / (D / 8)) * (16 * D / 8 / 32);
-            float qc = bf16f(qrows[c]);
-            for (uint32_t g2 = 1; g2 < L.G; ++g2) qc = __fadd_rn(qc, bf16f(qrows[g2 * D + c]));
+            constexpr uint32_t CPT = 16 * D / 8 / 32;  // codes per lane
+            const uint32_t c = warp * (D / 8) + (lane % (D / 8)), code0 = (lane / (D / 8)) * CPT;
+            const float qc = qsum(c), sc = scl[c], zp = zps[c], fc0 = float(code0);
 #pragma unroll
-            for (uint32_t k = 0; k < 16 * D / 8 / 32; ++k) {
-                const uint32_t code = code0 + k;
-                const float deq = asym ? __fadd_rn(zps[c], __fmul_rn(float(code), scl[c]))
-                                       : __fmul_rn(float(int(code) - 7), scl[c]);
-                tbl[c * 16 + code] = __fmul_rn(qc, deq);
+            for (uint32_t k = 0; k < CPT; ++k) {
+                const float fc = fc0 + float(k);  // exact small integers
+                const float deq = asym ? __fadd_rn(zp, __fmul_rn(fc, sc)) : __fmul_rn(fc - 7.0f, sc);
+                tbl[c * 16 + code0 + k] = __fmul_rn(qc, deq);
             }
         }
         SEL_TRACE(4);
@@ -604,8 +629,11 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             t_r = sh.st[1];
         }
         SEL_TRACE(6);
-        if (tid < Cn) st_cluster_u32(dsmem(&sh.slot[r], tid), t_r);  // every CTA gets every t_r
+        if (tid == 0) sh.st[5] = t_r;
     }
+    __syncthreads();
+    cluster_wait();  // every CTA of the cluster is initialised (phase 0)
+    if (tid < Cn) st_cluster_u32(dsmem(&sh.slot[r], tid), sh.st[5]);  // every CTA gets every t_r
     cluster_sync();  // #1: slices scored, bounds exchanged, product table complete
     SEL_TRACE(7);
 
@@ -695,6 +723,13 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     auto emit = [&](uint32_t p, uint32_t blk) {
         blocks[size_t(u) * stride + p] = blk;
         if (!pages.page) return;
+        if (trailing && blk == N - 1) {  // resolved at the start
+            for (uint32_t pp = 0; pp < ppb; ++pp) {
+                pages.page[pbase + size_t(p) * ppb + pp] = sh.tpg[pp];
+                pages.valid[pbase + size_t(p) * ppb + pp] = uint16_t(sh.tvl[pp]);
+            }
+            return;
+        }
         for (uint32_t pp = 0; pp < ppb; ++pp) {
             const uint32_t t0 = blk * du.block + pp * L.P;
             uint32_t v = 0, page = 0;
