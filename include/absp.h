@@ -245,6 +245,29 @@ absp_status absp_set_filter_diagnostics(absp_ctx* ctx, uint32_t layer, int enabl
 absp_status absp_download_filter_scores(absp_ctx* ctx, uint32_t layer, uint32_t seq, float* approx,
                                         float* err);
 
+/* full_attention_oracle (engine.cpp:357-403) on the GPU: exact dense decode
+ * attention of every query head over its sequence's whole cached context (the
+ * layer's bound KV; no store needed), in fp64 like the reference. out fp32
+ * [batch][Hq][d]. weights (optional, device fp64 [batch][Hq][weights_stride],
+ * weights_stride >= the longest sequence): AttentionOutput::weights, the softmax
+ * probabilities of every cached token (t < seq_len of the row's sequence).
+ * Logits are bit-exact (bf16 products are exact in fp64, serial channel order);
+ * the softmax denominator and the output sums are formed per split and merged, so
+ * weights and outputs agree with the reference to fp64 rounding. The dense side of
+ * the sparse/full A/B and the weight source of calibration. */
+absp_status absp_full_attention(absp_ctx* ctx, uint32_t layer, const void* q, float* out, double* weights,
+                                uint64_t weights_stride, void* stream);
+
+/* attention_recall (calibrator.cpp:48-71) per (sequence, q head): the fraction of
+ * the oracle's attention mass (weights from absp_full_attention, same layout) on
+ * tokens inside the selected blocks of the head's KV head (blocks / counts as
+ * absp_select writes them). recall: device fp64 [batch][Hq]. The per-KV-head
+ * recall of the reference (G = 1) is the q-head value; with GQA the calibrator
+ * averages the G heads of a group. */
+absp_status absp_attention_recall(absp_ctx* ctx, uint32_t layer, const double* weights, uint64_t weights_stride,
+                                  const uint32_t* blocks, uint32_t blocks_stride, const uint32_t* counts,
+                                  double* recall, void* stream);
+
 /* Deterministic counter-based N(0,1)-like bf16 generator used by the benchmark
  * and tests (same bytes as oracle/synth.py): element i of stream s gets
  * splitmix64(seed + golden * (s * 2^40 + i + 1)) -> Irwin-Hall(4 x u16) -> fp32

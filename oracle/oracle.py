@@ -86,6 +86,8 @@ def ref() -> C.CDLL:
         L.ref_seq_select_naive.argtypes = [C.c_void_p, _f32p, _sz, _u32p, _sz, _u32p]
         L.ref_seq_attend.argtypes = [C.c_void_p, _f32p, _f32p]
         L.ref_seq_full_attention.argtypes = [C.c_void_p, _f32p, _f32p]
+        L.ref_seq_full_attention_w.argtypes = [C.c_void_p, _f32p, _f32p,
+                                               np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
         L.ref_seq_decode_gqa.argtypes = [C.c_void_p, _f32p, _sz, _sz, _f32p]
         L.ref_engine_create.argtypes = [_sz, _sz, _sz, C.POINTER(_sz), _sz, _sz, C.c_int, C.c_int,
                                         C.c_int, C.POINTER(_sz), _sz, C.POINTER(C.c_void_p)]
@@ -336,6 +338,13 @@ class RefSeq:
         out = np.zeros((self.H, self.d), np.float32)
         _rcheck(ref().ref_seq_full_attention(self.h, np.ascontiguousarray(q, np.float32), out))
         return out
+
+    def full_attention_weights(self, q):
+        """full_attention_oracle: (output [H][d] fp32, weights [H][n] fp64)."""
+        out = np.zeros((self.H, self.d), np.float32)
+        w = np.zeros((self.H, self.n), np.float64)
+        _rcheck(ref().ref_seq_full_attention_w(self.h, np.ascontiguousarray(q, np.float32), out, w))
+        return out, w
 
     def decode_gqa(self, q_heads, G, token_budget) -> np.ndarray:
         out = np.zeros((self.H * G, self.d), np.float32)

@@ -220,6 +220,17 @@ int ref_seq_full_attention(void* h, const float* query, float* out) {
     });
 }
 
+// full_attention_oracle with its weights. query/out: [H][d]; weights: [H][n] fp64.
+int ref_seq_full_attention_w(void* h, const float* query, float* out, double* weights) {
+    return guard([&] {
+        const Seq* s = static_cast<Seq*>(h);
+        const size_t qn = s->store.num_heads * s->store.head_dim;
+        AttentionOutput o = full_attention_oracle(std::span<const float>(query, qn), *s->cache);
+        std::memcpy(out, o.output.data(), qn * sizeof(float));
+        std::memcpy(weights, o.weights.data(), o.weights.size() * sizeof(double));
+    });
+}
+
 // One GQA decode step per SURVEY.md Appendix A: q_group is [Hkv*G][d]
 // (q head hq = h*G + g). The KV-head query used for scoring is the left-to-right
 // fp32 group sum; attention runs once per group member. out: [Hkv*G][d].

@@ -305,6 +305,21 @@ class DecodeAttention:
         check(self._lib.absp_decode_step_host(self._ctx, layer, _ptr(q_host), _ptr(out_host),
                                               _stream(stream)))
 
+    def full_attention(self, layer: int, q, out, weights=None, stream=None) -> None:
+        """full_attention_oracle (engine.cpp:357-403) over each sequence's whole context:
+        out fp32 [batch][Hq][d]; weights (optional) fp64 [batch][Hq][stride], stride >= the
+        longest sequence, receives the softmax weights of every cached token."""
+        stride = int(weights.shape[-1]) if weights is not None else 0
+        check(self._lib.absp_full_attention(self._ctx, layer, _ptr(q), _ptr(out), _ptr(weights), stride,
+                                            _stream(stream)))
+
+    def attention_recall(self, layer: int, weights, blocks, counts, recall, stream=None) -> None:
+        """attention_recall (calibrator.cpp:48-71): recall fp64 [batch][Hq] = the weight mass on
+        tokens inside the selected blocks (blocks / counts as select() writes them)."""
+        check(self._lib.absp_attention_recall(self._ctx, layer, _ptr(weights), int(weights.shape[-1]),
+                                              _ptr(blocks), int(blocks.shape[-1]), _ptr(counts), _ptr(recall),
+                                              _stream(stream)))
+
     # -- introspection ---------------------------------------------------------
     def layer_info(self, layer: int) -> _abi.LayerInfo:
         info = _abi.LayerInfo()

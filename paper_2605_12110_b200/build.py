@@ -20,7 +20,7 @@ LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libabsp.so"
 OBJDIR = ROOT / "build" / "obj"
 
-SOURCES = ["api.cu", "engine.cu", "build_store.cu", "score.cu", "topk.cu", "select.cu", "attend.cu", "synth.cu"]
+SOURCES = ["api.cu", "engine.cu", "build_store.cu", "score.cu", "topk.cu", "select.cu", "attend.cu", "dense.cu", "synth.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
@@ -47,15 +47,26 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Pa
         return lib
     objdir.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(parents=True, exist_ok=True)
+    # an object is rebuilt when its source, a shared header or this script is newer
+    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "absp.h", Path(__file__)]
+    newest_header = max(f.stat().st_mtime for f in headers)
+    jobs = []
     objs = []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
+        objs.append(str(obj))
+        if (not force and obj.exists()
+                and obj.stat().st_mtime >= max(newest_header, (CSRC / src).stat().st_mtime)):
+            continue
         cmd = [nvcc(), *ARCH, *FLAGS, *(["-DABSP_ATTN_TRACE"] if trace else []), "-I", str(ROOT / "include"),
                "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+        jobs.append(cmd)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4) or 1) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c, check=True), jobs)):
+            pass
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     if verbose:

@@ -176,20 +176,44 @@ size_t attend_smem_bytes(uint32_t D, uint32_t P);
 // (sequence, KV head) unit in one kernel, one cluster of `cluster` CTAs per unit; the
 // same ordered selections as launch_score + launch_topk (INT4 mean stores).
 bool select_fused_supported(const LayerView& L);
+// One slice of the fused selection: rows [r nd / n, (r + 1) nd / n) of unit `unit`'s
+// candidate domain (nd = N, or N - 1 when the trailing block is forced), one CTA each;
+// `first` is the unit's first slice (its bounds are slot[first .. first + n)).
+struct SliceDesc {
+    uint32_t unit, r, n, first;
+};
 struct SelectPlan {
-    uint32_t cluster;    // CTAs per unit (thread-block cluster size)
+    uint32_t rows;       // slice size S (rows)
     uint32_t stages;     // code-ring stages (2..4)
-    uint32_t slice_cap;  // key slots per CTA (largest unit at capacity / cluster)
-    uint32_t cand_cap;   // candidates the leader orders
+    uint32_t cand_cap;   // candidates the finalize orders
+    uint32_t pg_cap;     // candidate page ids the finalize prefetches
+    uint32_t n_slices;   // grid
     bool ok;             // fits in shared memory
 };
-SelectPlan plan_select(uint32_t units, uint32_t max_cap_blocks, uint32_t max_budget, uint32_t D, int num_sms);
-size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t slice_cap, uint32_t cand_cap);
+struct SelectWork {
+    const SliceDesc* slices;  // [n_slices], unit order
+    uint32_t* slot;           // [2 n_slices] per-slice key range (min, max)
+    uint32_t* arrive;         // [units] slices done this step (zero between steps)
+    uint32_t* keys;           // [store segment] integer filter keys
+};
+SelectPlan plan_select(const std::vector<UnitDesc>& desc, uint32_t max_budget, uint32_t D, int num_sms,
+                       std::vector<SliceDesc>* slices);
+uint64_t select_slices_bound(const std::vector<UnitDesc>& desc);
+size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_t pg_cap);
 cudaError_t init_select_attributes();  // per device, once
-cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, uint32_t* blocks,
-                                uint32_t stride, uint32_t* counts, const PageList& pages, uint32_t* ready,
-                                float* diag_approx, float* diag_err, cudaStream_t s, int* launches);
+cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, const SelectWork& work,
+                                uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
+                                uint32_t* ready, float* diag_approx, float* diag_err, cudaStream_t s, int* launches);
 cudaError_t init_attend_attributes();  // per device, once
+// Dense fp64 decode attention with weights (dense.cu; full_attention_oracle,
+// engine.cpp:357-403) and attention_recall (calibrator.cpp:48-71).
+uint32_t full_attention_splits(uint32_t units, uint32_t max_tokens, int num_sms);
+cudaError_t launch_full_attention(const LayerView& L, const uint16_t* q, uint32_t splits, double* weights,
+                                  uint64_t wstride, double* part_o, double* part_ml, double* stats, float* out,
+                                  cudaStream_t s, int* launches);
+cudaError_t launch_recall(const LayerView& L, uint32_t max_nblocks, const double* weights, uint64_t wstride,
+                          const uint32_t* blocks, uint32_t stride, const uint32_t* counts, double* recall,
+                          cudaStream_t s, int* launches);
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);
 

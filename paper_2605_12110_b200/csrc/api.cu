@@ -226,12 +226,16 @@ struct Layer {
     TopkClasses topk_classes{};
     DevBuf<float> approx, unit_err;  // decode-step filter diagnostics: approximate scores, per-unit bounds
     bool filter_diag = false;        // the fused selection writes them (absp_set_filter_diagnostics)
-    SelectPlan sel_plan{};           // fused selection: cluster size, ring stages, capacities
+    SelectPlan sel_plan{};           // fused selection: slice size, ring stages, capacities, grid
+    DevBuf<SliceDesc> sel_slices;    // fused selection work (capacity-reserved at bind)
+    DevBuf<uint32_t> sel_slot, sel_arrive, sel_keys;
+    std::vector<SliceDesc> h_slices;
     DevBuf<float> qstat, qpart;     // frozen quantization statistics, build scratch
     DevBuf<uint32_t> wmask;         // decode-time maintenance: changed code words
     DevBuf<uint32_t> err_flags;     // explicit-selection validation (k_resolve_pages), kAttendErr*
     DevBuf<uint16_t> stage_q;
     DevBuf<float> stage_out;
+    DevBuf<double> full_o, full_ml, full_stats;  // absp_full_attention: split partials, (M, L) per q row
     // absp_decode_step_host as one CUDA graph: H2D q -> step kernels -> D2H out; the
     // copy nodes are re-pointed when the caller's host buffers change
     cudaGraph_t host_graph = nullptr;  // kept: the exec's copy nodes are addressed through it
@@ -259,9 +263,12 @@ struct Layer {
         codes.release(); codes_min.release();
         sel_blocks.release(); sel_counts.release(); ready.release(); scored.release(); topk_units.release();
         approx.release(); unit_err.release();
+        sel_slices.release(); sel_slot.release(); sel_arrive.release(); sel_keys.release();
+        h_slices.clear();
         qstat.release(); qpart.release(); wmask.release(); err_flags.release();
         stager.release();
         stage_q.release(); stage_out.release();
+        full_o.release(); full_ml.release(); full_stats.release();
         drop_host_graph();
         step_work.release();
         for (auto& kv : attend_work) kv.second.release();
@@ -530,10 +537,15 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
     ABSP_CUDA(l->scores.ensure(l->total_cap));
     ABSP_CUDA(l->approx.ensure(l->total_cap));
     ABSP_CUDA(l->unit_err.ensure(units));
+    std::vector<SliceDesc> slices;
+    l->sel_plan = plan_select(l->desc, l->max_budget, c.head_dim, ctx->num_sms, &slices);
     {
-        uint32_t max_cap_blocks = 0;
-        for (const UnitDesc& d : l->desc) max_cap_blocks = std::max(max_cap_blocks, d.cap);
-        l->sel_plan = plan_select(uint32_t(units), max_cap_blocks, l->max_budget, c.head_dim, ctx->num_sms);
+        const uint64_t bound = std::max<uint64_t>(select_slices_bound(l->desc), slices.size());
+        ABSP_CUDA(l->sel_slices.ensure(bound));
+        ABSP_CUDA(l->sel_slot.ensure(2 * bound));
+        ABSP_CUDA(l->sel_arrive.ensure(units));
+        ABSP_CUDA(l->sel_keys.ensure(l->total_cap + 8));  // + the TMA batches' 16-byte round-up
+        if (!async) ABSP_CUDA(cudaMemset(l->sel_arrive.p, 0, units * 4));
     }
     l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
@@ -550,7 +562,8 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
         for (const UnitDesc& d : l->desc)
             n_work_cap += std::max(chunks_for(std::min(std::max(d.n_blocks, d.cap), d.budget), d.block), 1u);
         const size_t bound = units * sizeof(UnitDesc) + (units + l->item_begin.size()) * sizeof(ScoreItem) +
-                             l->item_begin.size() * 4 + units * 4 * 3 + 2 * n_work_cap * 4 + 8 * 16 + 4096;
+                             l->item_begin.size() * 4 + units * 4 * 3 + 2 * n_work_cap * 4 + 8 * 16 + 4096 +
+                             select_slices_bound(l->desc) * sizeof(SliceDesc) + 16;
         ABSP_CUDA(up.reserve(bound));
     }
     ABSP_CUDA(up.begin(stream, async));
@@ -571,6 +584,10 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
         l->h_topk_order = order;
         l->topk_classes.units = l->topk_units.p;
     }
+    if (!async || slices.size() != l->h_slices.size() ||
+        std::memcmp(slices.data(), l->h_slices.data(), slices.size() * sizeof(SliceDesc)) != 0)
+        ABSP_CUDA(up.put(l->sel_slices.p, slices.data(), slices.size() * sizeof(SliceDesc)));
+    l->h_slices = slices;
     // explicit-selection work lists are rebuilt (in place) by their next absp_attend
     ++l->desc_version;
     st = build_work(*l, c.head_dim, c.page_size, true, 0, ctx->num_sms, l->step_work, &up, /*reserve=*/true);
@@ -582,7 +599,8 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
     // the decode step's layout-dependent kernel arguments
     std::vector<uint64_t> key = {l->step_work.n_work, l->step_work.grid, l->step_work.max_runs,
                                  l->item_begin.size(), topk_items(l->max_nblocks), l->max_nblocks > 0,
-                                 uint64_t(l->topk_classes.units != nullptr)};
+                                 uint64_t(l->topk_classes.units != nullptr), l->sel_plan.n_slices,
+                                 l->sel_plan.rows, l->sel_plan.stages, l->sel_plan.cand_cap, l->sel_plan.pg_cap};
     for (int cls = 0; cls <= kTopkClasses; ++cls) key.push_back(l->topk_classes.begin[cls]);
     if (key != l->step_key) {
         l->step_key = key;
@@ -926,6 +944,60 @@ absp_status absp_attend_validate(absp_ctx* ctx, uint32_t layer, void* stream) {
     return ABSP_OK;
 }
 
+absp_status absp_full_attention(absp_ctx* ctx, uint32_t layer, const void* q, float* out, double* weights,
+                                uint64_t weights_stride, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->bound) return fail(ABSP_ESTATE, "full_attention: call absp_kv_bind first");
+    if (!q || !out) return fail(ABSP_EINVAL, "full_attention: null pointer");
+    uint32_t max_len = 0;
+    for (uint32_t n : l->seq_lens) max_len = std::max(max_len, n);
+    if (weights && weights_stride < max_len)
+        return fail(ABSP_EINVAL, "full_attention: weights_stride " + std::to_string(weights_stride) +
+                                     " < longest sequence " + std::to_string(max_len));
+    const absp_config& c = ctx->cfg;
+    DeviceGuard dg(ctx->device);
+    const LayerView v = view_of(ctx, *l);
+    const uint32_t splits = full_attention_splits(v.units, max_len, ctx->num_sms);
+    const size_t parts = size_t(v.units) * splits * v.G;
+    const size_t rows = size_t(l->batch) * c.num_q_heads;
+    if (l->full_o.n < parts * c.head_dim || l->full_stats.n < rows * 2) {
+        // first use (or a larger layout): allocation synchronises with the device
+        ABSP_CUDA(cudaDeviceSynchronize());
+        ABSP_CUDA(l->full_o.ensure(parts * c.head_dim));
+        ABSP_CUDA(l->full_ml.ensure(parts * 2));
+        ABSP_CUDA(l->full_stats.ensure(rows * 2));
+    }
+    int n = 0;
+    cudaError_t e = launch_full_attention(v, static_cast<const uint16_t*>(q), splits, weights, weights_stride,
+                                          l->full_o.p, l->full_ml.p, l->full_stats.p, out, cudaStream_t(stream), &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "full_attention kernels");
+    return ABSP_OK;
+}
+
+absp_status absp_attention_recall(absp_ctx* ctx, uint32_t layer, const double* weights, uint64_t weights_stride,
+                                  const uint32_t* blocks, uint32_t blocks_stride, const uint32_t* counts,
+                                  double* recall, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->bound) return fail(ABSP_ESTATE, "attention_recall: call absp_kv_bind first");
+    if (!weights || !blocks || !counts || !recall) return fail(ABSP_EINVAL, "attention_recall: null pointer");
+    uint32_t max_len = 0;
+    for (uint32_t n : l->seq_lens) max_len = std::max(max_len, n);
+    if (weights_stride < max_len || blocks_stride == 0)
+        return fail(ABSP_EINVAL, "attention_recall: mismatched oracle/selection shapes");  // calibrator.cpp:51-55
+    DeviceGuard dg(ctx->device);
+    int n = 0;
+    cudaError_t e = launch_recall(view_of(ctx, *l), l->max_nblocks, weights, weights_stride, blocks, blocks_stride,
+                                  counts, recall, cudaStream_t(stream), &n);
+    ctx->launches += n;
+    if (e != cudaSuccess) return cuda_fail(e, "attention_recall kernel");
+    return ABSP_OK;
+}
+
 uint64_t absp_layout_version(absp_ctx* ctx, uint32_t layer) {
     if (!ctx || layer >= ctx->layers.size()) return 0;
     return ctx->layers[layer].layout_version;
@@ -944,7 +1016,8 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     if (!ctx->exact_select && select_fused_supported(v) && l->sel_plan.ok) {
         // fused filter + exact refine + top-k + page resolution, one cluster per unit
         int n = 0;
-        cudaError_t e = launch_select_fused(v, static_cast<const uint16_t*>(q), l->sel_plan, l->sel_blocks.p,
+        const SelectWork sw{l->sel_slices.p, l->sel_slot.p, l->sel_arrive.p, l->sel_keys.p};
+        cudaError_t e = launch_select_fused(v, static_cast<const uint16_t*>(q), l->sel_plan, sw, l->sel_blocks.p,
                                             l->sel_stride, l->sel_counts.p, l->step_work.pages(), l->ready.p,
                                             l->filter_diag ? l->approx.p : nullptr,
                                             l->filter_diag ? l->unit_err.p : nullptr, s, &n);

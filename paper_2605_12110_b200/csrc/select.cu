@@ -1,11 +1,16 @@
 // Fused decode-step selection (sm_100a): estimate_scores + select_topk +
-// populate_page_spans (engine.cpp:34-97, 119-178, 271-283) for INT4 mean stores in
-// ONE kernel, one thread-block cluster of C CTAs per (sequence, KV head) unit, with
-// the same ordered block lists the reference computes (bit-exact), but without the
-// serial fp32 score of every centroid.
+// populate_page_spans (engine.cpp:34-97, 119-178, 271-283) for INT4 mean stores,
+// with the same ordered block lists the reference computes (bit-exact), but without
+// the serial fp32 score of every centroid.
 //
-//   stream  : the producer warp bulk-copies (TMA) the CTA's slice of the unit's packed
-//             code rows into a 4-stage ring, plus q and the unit's scale / zero point.
+// Work is cut into SLICES of at most S consecutive centroids of one (sequence, KV
+// head) unit (S picked per layout so that the slices fill about two CTAs per SM), one
+// CTA per slice, slices in unit order: every CTA streams about the same number of code
+// bytes whatever the block sizes, and the last slice of a unit to finish completes
+// its selection (no cluster, no inter-CTA waiting):
+//
+//   stream  : the producer warp bulk-copies (TMA) the slice's packed code rows into a
+//             4-stage ring, plus q and the unit's scale / zero point.
 //   filter  : consumers compute, per centroid, the exact integer
 //                 I_i = sum_c (256 h_c + l_c) code_ic   (codes 0..15, integer tensor cores:
 //                 mma.sync m16n8k32 u8 x s8 -> s32 on code words fed by ldmatrix, even
@@ -18,21 +23,23 @@
 //             bounds the products; the serial sum of 128 rounded products is within
 //             ~131u M of the real sum, so 2^-14 keeps an 8x margin; the second term is
 //             the weight quantisation exactly, codes <= 15). In integer units
-//             E_int = ceil(E 256 / sigma) + 2.
-//   bound   : every CTA finds a lower bound t_r of the ceil((K-1)/C)-th largest of its
-//             slice's I (a 1024-bin histogram); T = min_r t_r (DSMEM exchange) is a lower
-//             bound of the (K-1)-th largest I of the unit. Any block of the exact
-//             top-(K-1) has I >= T - 2 E_int (else K-1 blocks score strictly higher), so
-//             the candidates {I_i >= T - 2 E_int} (typically K-1 plus a few) contain it.
-//   refine  : each CTA scores its candidates with the reference's exact serial fp32
-//             arithmetic (product table, score.cu) and sends (key << 32 | ~index)
-//             composites to the leader CTA's shared memory (DSMEM); the leader orders
-//             them, keeps the top K-1, inserts the trailing block N-1 (forced, exactly
-//             where its exact score ranks), and publishes blocks, counts, the page list
-//             and the unit's ready flag for the attention producer (common.cuh).
-//   fallback: more candidates than fit (mass ties) -> the leader scores every block
-//             exactly into the scores buffer and runs an exact radix select (slow, rare,
-//             identical result).
+//             E_int = ceil(E 256 / sigma) + 2. Every slice derives the same weights.
+//   bound   : each slice r of the unit's C slices finds a lower bound t_r of the
+//             ceil((K-1)/C)-th largest I of its rows (a 1024-bin histogram) and writes
+//             its keys and t_r to global memory; T = min_r t_r is a lower bound of the
+//             (K-1)-th largest I of the unit. Any block of the exact top-(K-1) has
+//             I >= T - 2 E_int (else K-1 blocks score strictly higher), so the
+//             candidates {I_i >= T - 2 E_int} (typically K-1 plus a few) contain it.
+//   finalize: the slice CTA that arrives last on the unit's counter (acq_rel) scans the
+//             unit's keys (L2), scores the candidates with the reference's exact serial
+//             fp32 arithmetic (product table, score.cu), ranks the composites
+//             (key << 32 | ~index), keeps the top K-1, inserts the trailing block N-1
+//             (forced, exactly where its exact score ranks), and publishes blocks,
+//             counts, the page list and the unit's ready flag for the attention
+//             producer (common.cuh).
+//   fallback: more candidates than fit (mass ties) -> the finalizing CTA scores every
+//             block exactly into the scores buffer and runs an exact radix select
+//             (slow, rare, identical result).
 #include "absp_internal.cuh"
 #include "common.cuh"
 #include "ptx.cuh"
@@ -51,15 +58,20 @@ constexpr int kSRows = kSCons;           // rows per stage
 constexpr int kSStages = 4;
 constexpr uint32_t kCandCapMax = 2048;   // candidate capacity bound (>= K, K <= T / min B <= 2048)
 constexpr int kBins = 1024;
+constexpr uint32_t kNoPrefetch = 0xfffffffeu;  // emit: resolve the block's pages from the page table
+constexpr uint32_t kSliceMin = 256;      // slice rows: a multiple of kSliceMin ...
+constexpr uint32_t kSliceMax = 4096;     // ... up to this
+constexpr uint32_t kFinKeys = 8192;      // finalize: keys per TMA batch in shared memory
+constexpr uint32_t kRefineMin = 48;      // finalize: keys in the threshold bin above which it is refined
 
 // Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
 // globaltimer stamps at the phase boundaries (tools/select_trace.py).
 #ifdef ABSP_ATTN_TRACE
 constexpr int kSelTraceSlots = 16;
-__device__ unsigned long long g_sel_trace[2048 * kSelTraceSlots];
+__device__ unsigned long long g_sel_trace[4096 * kSelTraceSlots];
 #define SEL_TRACE(slot)                                                                           \
     do {                                                                                          \
-        if (threadIdx.x == 0 && blockIdx.x < 2048) {                                              \
+        if (threadIdx.x == 0 && blockIdx.x < 4096) {                                              \
             unsigned long long t_;                                                                \
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                 \
             g_sel_trace[blockIdx.x * kSelTraceSlots + (slot)] = t_;                               \
@@ -79,21 +91,18 @@ struct SelCfg {
     static constexpr int TBL = D * 16 * 4; // exact product table
 };
 
-// Fixed-size part of the shared memory; the candidate arrays follow it:
-//   cand [cand_cap] u64 (leader: composites), list / outs [cand_cap] u32 (this CTA's
-//   candidate indices, then the leader's ordered selection).
+// Fixed-size part of the shared memory (after the ring, keys, table and parameters).
 struct SelHead {
-    unsigned long long bars[2 * kSStages + 1];  // full[NS], empty[NS], params
+    unsigned long long bars[2 * kSStages + 2];  // full[NS], empty[NS], params, finalize keys
+    unsigned long long ct;               // finalize: the trailing block's composite
     int8_t hlw[kSCons / 32][2][128];     // per consumer warp: h and l per channel (D <= 128)
-    uint32_t tpg[kAttnChunkRows];        // leader: the trailing block's pool pages (prefetched)
-    uint32_t tvl[kAttnChunkRows];        //         and their valid rows
     float red[4][kSWarps];       // block reductions
-    uint32_t slot[8];            // per-rank local bounds t_r (written by every CTA of the cluster)
+    uint32_t tpg[kAttnChunkRows];  // finalize: the trailing block's pool pages
     uint32_t st[16];             // misc scalars
-    uint32_t hist[kBins];
-    uint32_t local_cnt;
-    uint32_t cand_cnt;           // leader: composites received
-    uint32_t overflow;           // leader: some CTA could not deliver all its candidates
+    alignas(16) uint32_t hist[kBins];
+    uint32_t local_cnt;          // finalize: candidates found
+    uint32_t cand_cnt;
+    uint32_t overflow;
     uint32_t nsel;
     unsigned long long* cand;
     uint32_t* list;
@@ -101,45 +110,6 @@ struct SelHead {
     uint32_t cap;
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_size() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void cluster_arrive() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-// Address of `p` (this CTA's shared memory) in CTA `rank` of the cluster.
-__device__ __forceinline__ uint32_t dsmem(const void* p, uint32_t rank) {
-    uint32_t a;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
-    return a;
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster_u64(uint32_t addr, unsigned long long v) {
-    asm volatile("st.shared::cluster.u64 [%0], %1;\n" ::"r"(addr), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t atom_add_cluster(uint32_t addr, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;\n" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-    return old;
-}
-__device__ __forceinline__ void red_or_cluster(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared::cluster.or.b32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
-}
 __device__ __forceinline__ void cons_sync() {  // named barrier 1: the consumer warps
     asm volatile("bar.sync 1, %0;\n" ::"n"(kSCons) : "memory");
 }
@@ -299,21 +269,6 @@ __device__ void exact_fallback(const LayerView& L, const UnitDesc& du, SelHead& 
     order_selection(sh, K1, K, true, ct, N);
 }
 
-// Shared-memory layout (host and device): ring [stages][rows][row bytes] | keys
-// [slice_cap] | product table | q rows | scales, zps | SelHead | cand | list/outs.
-template <int D>
-struct SelLayout {
-    size_t keys, tbl, prm, head, cand, list, total;
-    __host__ __device__ SelLayout(uint32_t stages, uint32_t slice_cap, uint32_t cand_cap) {
-        keys = size_t(stages) * SelCfg<D>::STAGEB;
-        tbl = keys + ((size_t(slice_cap) * 4 + 15) & ~size_t(15));
-        prm = tbl + SelCfg<D>::TBL;
-        head = prm + SelCfg<D>::QB + SelCfg<D>::PB;
-        cand = (head + sizeof(SelHead) + 15) & ~size_t(15);
-        list = cand + size_t(cand_cap) * 8;
-        total = list + size_t(cand_cap) * 4;
-    }
-};
 
 // Integer MMA: C[16x8] (s32) += A[16x32] (u8, row) * B[32x8] (s8, col), exact.
 __device__ __forceinline__ void imma(int* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -330,29 +285,87 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r
                  : "r"(addr));
 }
 
+// Warp: the bin of hist[0, 1024) holding the kr-th largest element counted from the top
+// bin (1 <= kr <= total). Lane l sums bins [32 l, 32 l + 32) (8 16-byte loads in a
+// lane-rotated order: conflict-free), a suffix scan over the lanes finds the lane L
+// holding it, and a second suffix scan over L's 32 bins (one per lane) the bin. Writes
+// the bin and the number of elements in the bins above it.
+__device__ __forceinline__ void find_bin_desc(const uint32_t* hist, uint32_t kr, uint32_t lane, uint32_t* bin,
+                                              uint32_t* above) {
+    uint32_t tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint4 x = *reinterpret_cast<const uint4*>(hist + lane * 32 + ((uint32_t(k) + lane) & 7u) * 4);
+        tot += (x.x + x.y) + (x.z + x.w);
+    }
+    uint32_t incl = tot;  // elements in lanes >= this one (larger bins)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += x;
+    }
+    const uint32_t hit = __ballot_sync(0xffffffffu, incl - tot < kr && kr <= incl);
+    const uint32_t L = __ffs(hit) - 1;
+    const uint32_t cumL = __shfl_sync(0xffffffffu, incl - tot, L);  // elements above lane L's bins
+    const uint32_t c = hist[L * 32 + lane];
+    uint32_t in2 = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_down_sync(0xffffffffu, in2, o);
+        if (lane + o < 32) in2 += x;
+    }
+    const uint32_t hit2 = __ballot_sync(0xffffffffu, cumL + in2 - c < kr && kr <= cumL + in2);
+    const uint32_t i = __ffs(hit2) - 1;
+    if (lane == i) {
+        *bin = L * 32 + i;
+        *above = cumL + in2 - c;
+    }
+}
+
+// Shared-memory layout (host and device): ring [stages][rows][row bytes] (in the
+// finalize: the candidate composites cand [cand_cap] u64, list / outs [cand_cap] u32, the
+// candidates' prefetched pages cpg [pg_cap] u32 and a batch of the unit's keys) | product
+// table | q rows | scales, zps | SelHead.
 template <int D>
-__global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint16_t* __restrict__ q, uint32_t stages,
-                                                       uint32_t slice_cap, uint32_t cand_cap, uint32_t* blocks,
-                                                       uint32_t stride, uint32_t* counts, PageList pages,
-                                                       uint32_t* ready, float* diag_approx, float* diag_err) {
+struct SelLayout {
+    size_t cand, list, cpg, fkeys, tbl, prm, head, total;
+    __host__ __device__ SelLayout(uint32_t stages, uint32_t cand_cap, uint32_t pg_cap) {
+        cand = 0;
+        list = size_t(cand_cap) * 8;
+        cpg = list + size_t(cand_cap) * 4;
+        fkeys = (cpg + size_t(pg_cap) * 4 + 15) & ~size_t(15);
+        const size_t ring = size_t(stages) * SelCfg<D>::STAGEB, fin = fkeys + (kFinKeys + 8) * 4;
+        tbl = ((ring > fin ? ring : fin) + 15) & ~size_t(15);
+        prm = tbl + SelCfg<D>::TBL;
+        head = prm + SelCfg<D>::QB + SelCfg<D>::PB;
+        total = (head + sizeof(SelHead) + 15) & ~size_t(15);
+    }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint16_t* __restrict__ q, SelectPlan plan,
+                                                       SelectWork sw, uint32_t* blocks, uint32_t stride,
+                                                       uint32_t* counts, PageList pages, uint32_t* ready,
+                                                       float* diag_approx, float* diag_err) {
     using C = SelCfg<D>;
     constexpr int W = C::W, NG = D / 32;  // code words per row, 16-byte groups (32 channels) per row
     extern __shared__ __align__(1024) unsigned char smem[];
-    const SelLayout<D> lay(stages, slice_cap, cand_cap);
+    const uint32_t stages = plan.stages, cand_cap = plan.cand_cap;
+    const SelLayout<D> lay(stages, cand_cap, plan.pg_cap);
     unsigned char* ring = smem;
-    uint32_t* keys = reinterpret_cast<uint32_t*>(smem + lay.keys);  // [slice_cap]
     float* tbl = reinterpret_cast<float*>(smem + lay.tbl);          // [D][16]
     unsigned char* prm_raw = smem + lay.prm;                         // q rows | scales | zps
     SelHead& sh = *reinterpret_cast<SelHead*>(smem + lay.head);
     const uint16_t* qrows = reinterpret_cast<const uint16_t*>(prm_raw);
     const float* scl = reinterpret_cast<const float*>(prm_raw + C::QB);
     const float* zps = scl + D;
-    unsigned long long* cand = reinterpret_cast<unsigned long long*>(smem + lay.cand);
+    unsigned long long* cand = reinterpret_cast<unsigned long long*>(smem + lay.cand);  // finalize (ring)
     uint32_t* list = reinterpret_cast<uint32_t*>(smem + lay.list);
+    uint32_t* cpg = reinterpret_cast<uint32_t*>(smem + lay.cpg);                        // finalize (ring)
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t Cn = cluster_size(), r = cluster_rank();
-    const uint32_t u = blockIdx.x / Cn;
+    const SliceDesc sd = sw.slices[blockIdx.x];
+    const uint32_t u = sd.unit, r = sd.r, Cn = sd.n;
     const UnitDesc du = L.desc[u];
     const uint32_t N = du.n_blocks, K = du.budget;
     const bool all = N <= K;               // every block selected (ordered)
@@ -360,8 +373,8 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     const uint32_t s0 = uint32_t((uint64_t(r) * nd) / Cn), s1 = uint32_t((uint64_t(r + 1) * nd) / Cn);
     const uint32_t ns = s1 - s0;
     const uint32_t n_chunks = (ns + kSRows - 1) / kSRows;
-    const bool resident = n_chunks <= stages;  // the whole slice stays in the ring
-    const bool trailing = !all;                // block N-1 is forced in (scored by the leader)
+    const bool trailing = !all;            // block N-1 is forced in (scored by the finalize)
+    uint32_t* gkeys = sw.keys + du.seg;
 
     SEL_TRACE(0);
     if (tid == 0) {
@@ -374,6 +387,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             mbar_init(smem_u32(&sh.bars[kSStages + i]), kSCons / 32);
         }
         mbar_init(smem_u32(&sh.bars[2 * kSStages]), 1);
+        mbar_init(smem_u32(&sh.bars[2 * kSStages + 1]), 1);
         mbar_fence_init();
         sh.local_cnt = 0u;
         sh.cand_cnt = 0u;
@@ -382,35 +396,31 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         sh.st[1] = 0u;
     }
     for (uint32_t i = tid; i < uint32_t(kBins); i += kSThreads) sh.hist[i] = 0u;
-    {   // the page resolution at the end reads the sequence's page-table row: warm L2
+    if (r + 1 == Cn) {  // the page resolution of the finalize reads the sequence's page-table row: warm L2
         const uint32_t row_pages = (du.n_tokens + L.P - 1) / L.P;
         const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
-        const uint32_t a = uint32_t((uint64_t(r) * row_pages) / Cn), b = uint32_t((uint64_t(r + 1) * row_pages) / Cn);
-        for (uint32_t p = a + tid * 32; p < b; p += kSThreads * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pt + p));
+        for (uint32_t p = tid * 32; p < row_pages; p += kSThreads * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pt + p));
     }
     __syncthreads();
     griddep_wait();  // codes / params (appends) and q are written by earlier kernels
     // The attention kernel may be scheduled now: every CTA of this grid is past its wait,
     // i.e. the previous step's attention has completed (its merges re-armed the ready flags).
     griddep_launch_dependents();
-    // the leader's last thread fetches the trailing block's code row now; it is scored
-    // exactly once the product table exists (after barrier #1)
-    uint32_t trail[W];
-    if (r == 0 && trailing && tid == kSThreads - 1) load_row_global<W>(L.codes, du.seg + N - 1, N - 1, trail);
-    if (r == 0 && trailing && warp == kSWarps - 1 && pages.page) {  // and its pages
-        const uint32_t ppb = du.block / L.P;
-        const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
-        for (uint32_t pp = lane; pp < ppb; pp += 32) {
-            const uint32_t t0 = (N - 1) * du.block + pp * L.P;
-            sh.tvl[pp] = t0 < du.n_tokens ? min(L.P, du.n_tokens - t0) : 0u;
-            sh.tpg[pp] = t0 < du.n_tokens ? du.head * uint32_t(L.pool_pages) + __ldg(pt + t0 / L.P) : 0u;
-        }
-    }
     SEL_TRACE(1);
-    // this CTA's shared memory is initialised: no CTA of the cluster touches another's
-    // before the matching wait (just before the first DSMEM access, after the filter)
-    cluster_arrive();
-    SEL_TRACE(2);
+
+    const uint32_t G = L.G;
+    // q_c = left-to-right fp32 group sum (score.cu)
+    auto qsum = [&](uint32_t c) {
+        float qg[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) qg[g] = uint32_t(g) < G ? bf16f(qrows[g * D + c]) : 0.0f;  // independent loads
+        float qc = qg[0];
+#pragma unroll
+        for (int g = 1; g < 8; ++g)
+            if (uint32_t(g) < G) qc = __fadd_rn(qc, qg[g]);
+        return qc;
+    };
+    const bool asym = L.mode == ABSP_QUANT_ASYM;
 
     if (warp == kSWarps - 1) {
         // =============================== producer ===============================
@@ -431,25 +441,15 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             }
         }
         __syncwarp();
+        if (lane == 0) mbar_wait(smem_u32(&sh.bars[2 * kSStages]), 0);  // parameters landed (finalize reads them)
+        __syncwarp();
     } else {
         // =============================== consumers ==============================
         mbar_wait(smem_u32(&sh.bars[2 * kSStages]), 0);
         SEL_TRACE(3);
-        const bool asym = L.mode == ABSP_QUANT_ASYM;
         // Every warp derives the weights itself (identical arithmetic, no CTA barrier):
-        // lane owns channels lane + 32 j. q_c = left-to-right fp32 group sum (score.cu).
+        // lane owns channels lane + 32 j.
         constexpr int CPL = D / 32;
-        const uint32_t G = L.G;
-        auto qsum = [&](uint32_t c) {
-            float qg[8];
-#pragma unroll
-            for (int g = 0; g < 8; ++g) qg[g] = uint32_t(g) < G ? bf16f(qrows[g * D + c]) : 0.0f;  // independent loads
-            float qc = qg[0];
-#pragma unroll
-            for (int g = 1; g < 8; ++g)
-                if (uint32_t(g) < G) qc = __fadd_rn(qc, qg[g]);
-            return qc;
-        };
         float wv[CPL];
         float wmax = 0.0f, M = 0.0f;
 #pragma unroll
@@ -513,18 +513,6 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             bfr[G][0] = gq < 2 ? v : 0u;
             bfr[G][1] = (gq >= 2 && gq < 4) ? v : 0u;
         }
-        // exact product table (for the refine): this warp's 16 channels x 16 codes
-        {
-            constexpr uint32_t CPT = 16 * D / 8 / 32;  // codes per lane
-            const uint32_t c = warp * (D / 8) + (lane % (D / 8)), code0 = (lane / (D / 8)) * CPT;
-            const float qc = qsum(c), sc = scl[c], zp = zps[c], fc0 = float(code0);
-#pragma unroll
-            for (uint32_t k = 0; k < CPT; ++k) {
-                const float fc = fc0 + float(k);  // exact small integers
-                const float deq = asym ? __fadd_rn(zp, __fmul_rn(fc, sc)) : __fmul_rn(fc - 7.0f, sc);
-                tbl[c * 16 + code0 + k] = __fmul_rn(qc, deq);
-            }
-        }
         SEL_TRACE(4);
 
         // ---- filter: exact integer scores I_i of the slice on the tensor cores ----
@@ -560,37 +548,33 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
                     const uint32_t ra = row0 + gq, rb = ra + 8;
                     if (ra < ns) {
                         const uint32_t k = uint32_t(I0) ^ 0x80000000u;
-                        keys[ra] = k;
+                        __stcg(gkeys + s0 + ra, k);
                         kmin = min(kmin, k);
                         kmax = max(kmax, k);
                         if (diag_approx) diag_approx[du.seg + s0 + ra] = float(I0) * a_scale;
                     }
                     if (rb < ns) {
                         const uint32_t k = uint32_t(I1) ^ 0x80000000u;
-                        keys[rb] = k;
+                        __stcg(gkeys + s0 + rb, k);
                         kmin = min(kmin, k);
                         kmax = max(kmax, k);
                         if (diag_approx) diag_approx[du.seg + s0 + rb] = float(I1) * a_scale;
                     }
                 }
             }
-            if (!resident) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&sh.bars[kSStages + stg]));
-            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&sh.bars[kSStages + stg]));
         }
         SEL_TRACE(5);
-        // ---- local lower bound t_r of the k_r-th largest: 1024 bins of the key range ----
-        uint32_t t_r = 0u;
-        const uint32_t kr = (K - 1 + Cn - 1) / Cn;
-        if (!all && K > 1 && ns >= kr) {
-            kmin = __reduce_min_sync(0xffffffffu, kmin);
-            kmax = __reduce_max_sync(0xffffffffu, kmax);
-            if (lane == 0) {
-                sh.red[0][warp] = __uint_as_float(kmin);
-                sh.red[1][warp] = __uint_as_float(kmax);
-            }
-            cons_sync();
+        // ---- the slice's key range for the unit's finalize ----
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        kmax = __reduce_max_sync(0xffffffffu, kmax);
+        if (lane == 0) {
+            sh.red[0][warp] = __uint_as_float(kmin);
+            sh.red[1][warp] = __uint_as_float(kmax);
+        }
+        cons_sync();
+        if (tid == 0) {
             kmin = 0xffffffffu;
             kmax = 0u;
 #pragma unroll
@@ -598,114 +582,194 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
                 kmin = min(kmin, __float_as_uint(sh.red[0][i]));
                 kmax = max(kmax, __float_as_uint(sh.red[1][i]));
             }
-            const uint32_t span = kmax - kmin;  // bins: (key - kmin) >> shift < 1024
-            const uint32_t shift = span < uint32_t(kBins) ? 0u : 32u - __clz(span) - 10u;
-            for (uint32_t i = tid; i < ns; i += kSCons) atomicAdd(&sh.hist[(keys[i] - kmin) >> shift], 1u);
-            cons_sync();
-            if (warp == 0) {  // bin holding the kr-th largest, counted from the top
-                constexpr int PER = kBins / 32;
-                uint32_t tot = 0;
-#pragma unroll 8
-                for (int j = 0; j < PER; ++j) tot += sh.hist[kBins - 1 - (lane * PER + j)];
-                uint32_t incl = tot;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= uint32_t(o)) incl += v;
-                }
-                uint32_t cum = incl - tot;
-                if (cum < kr && kr <= incl) {
-                    for (int j = 0; j < PER; ++j) {
-                        const uint32_t b = kBins - 1 - (lane * PER + j);
-                        cum += sh.hist[b];
-                        if (cum >= kr) {  // every key of bin b and above is >= its lower edge
-                            sh.st[1] = kmin + (b << shift);
-                            break;
-                        }
-                    }
-                }
-            }
-            cons_sync();
-            t_r = sh.st[1];
+            __stcg(sw.slot + 2 * blockIdx.x, kmin);
+            __stcg(sw.slot + 2 * blockIdx.x + 1, kmax);
         }
         SEL_TRACE(6);
-        if (tid == 0) sh.st[5] = t_r;
     }
     __syncthreads();
-    cluster_wait();  // every CTA of the cluster is initialised (phase 0)
-    if (tid < Cn) st_cluster_u32(dsmem(&sh.slot[r], tid), sh.st[5]);  // every CTA gets every t_r
-    cluster_sync();  // #1: slices scored, bounds exchanged, product table complete
+    // the last slice of the unit to arrive finalizes it (acq_rel: every slice's keys and
+    // bound, published before its arrival, are visible after ours)
+    if (tid == 0) {
+        uint32_t old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(sw.arrive + u) : "memory");
+        sh.st[6] = old + 1 == Cn;
+        if (old + 1 == Cn) sw.arrive[u] = 0u;  // re-armed for the next step (every slice has arrived)
+    }
+    __syncthreads();
     SEL_TRACE(7);
+    if (!sh.st[6]) return;
+    __threadfence();
 
-    // ---- candidates of this slice, exact scores, composites to the leader ----
-    if (r == 0 && trailing && tid == kSThreads - 1) sh.st[3] = order_key(exact_row<W>(trail, tbl));
+    // ================================ finalize ==================================
+    // Kept compact on purpose: the finalize runs once per unit on cold instruction caches
+    // (a step streams more than L2 holds), so its time follows the instruction bytes it
+    // traverses. Loops stay rolled; the unit's keys arrive by one TMA bulk copy per
+    // batch of kFinKeys.
+    const uint32_t ppb = du.block / L.P;
+    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
+    const uint32_t head_base = du.head * uint32_t(L.pool_pages);
+    uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + lay.fkeys);
+    const uint32_t kbar = smem_u32(&sh.bars[2 * kSStages + 1]);
+    uint32_t kphase = 0;
+    // keys [k0, min(k0 + kFinKeys, nd)) -> skeys[off ..]; every thread waits for them
+    auto fetch_keys = [&](uint32_t k0) -> uint32_t {
+        const uint32_t k1 = min(nd, k0 + kFinKeys);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(gkeys + k0);
+        const uint32_t off = uint32_t(a & 15u) / 4;
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy keys -> TMA reads
+            const uint32_t bytes = ((k1 - k0 + off) * 4 + 15) & ~15u;
+            mbar_expect_tx(kbar, bytes);
+            bulk_g2s(smem_u32(skeys), reinterpret_cast<const void*>(a & ~uintptr_t(15)), bytes, kbar);
+        }
+        return off;
+    };
+    auto wait_keys = [&]() {
+        mbar_wait(kbar, kphase & 1u);
+        ++kphase;
+    };
+    uint32_t koff = fetch_keys(0);
+    if (warp == kSWarps - 1) {  // the unit's key range: min / max over its slices
+        uint32_t mn = 0xffffffffu, mx = 0u;
+        for (uint32_t i = lane; i < Cn; i += 32) {
+            mn = min(mn, __ldcg(sw.slot + 2 * (sd.first + i)));
+            mx = max(mx, __ldcg(sw.slot + 2 * (sd.first + i) + 1));
+        }
+        mn = __reduce_min_sync(0xffffffffu, mn);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) {
+            sh.st[7] = mn;
+            sh.st[8] = mx;
+        }
+    } else {  // exact product table: warp w < 8 builds 16 channels x 16 codes
+        constexpr uint32_t CPT = 16 * D / 8 / 32;  // codes per lane
+        const uint32_t c = warp * (D / 8) + (lane % (D / 8)), code0 = (lane / (D / 8)) * CPT;
+        const float qc = qsum(c), sc = scl[c], zp = zps[c], fc0 = float(code0);
+#pragma unroll 1
+        for (uint32_t k = 0; k < CPT; ++k) {
+            const float fc = fc0 + float(k);  // exact small integers
+            const float deq = asym ? __fadd_rn(zp, __fmul_rn(fc, sc)) : __fmul_rn(fc - 7.0f, sc);
+            tbl[c * 16 + code0 + k] = __fmul_rn(qc, deq);
+        }
+    }
+    wait_keys();
+    __syncthreads();  // key range, table, first keys
+    SEL_TRACE(2);
     const uint32_t e_int = sh.st[0];
+    const bool one_batch = nd <= kFinKeys;
     uint32_t thr = 0u;
     if (!all && K > 1) {
-        uint32_t T = 0xffffffffu;
-        for (uint32_t i = 0; i < Cn; ++i) T = min(T, sh.slot[i]);
-        thr = (e_int == 0xffffffffu || T < 2ull * e_int) ? 0u : T - 2u * e_int;
+        // T = lower edge of the histogram bin holding the (K-1)-th largest key, refined once
+        // inside that bin: at least K-1 keys are >= T (a lower bound of the (K-1)-th largest;
+        // exact when the second-level bins are one key value wide)
+        const uint32_t kmin = sh.st[7], span = sh.st[8] - kmin;
+        const uint32_t shift = span < uint32_t(kBins) ? 0u : 32u - __clz(span) - 10u;
+        uint32_t lo = kmin, sh1 = shift, kr = K - 1, bin0 = 0xffffffffu;
+        for (int level = 0; level < 2; ++level) {
+            // level 0: every key; level 1: the keys of bin0, sub-bins of width 2^sh1
+            for (uint32_t b0 = 0; b0 < nd; b0 += kFinKeys) {
+                if (b0 > 0) {
+                    __syncthreads();
+                    koff = fetch_keys(b0);
+                    wait_keys();
+                }
+                const uint32_t nb = min(kFinKeys, nd - b0);
+#pragma unroll 4
+                for (uint32_t i = tid; i < nb; i += kSThreads) {
+                    const uint32_t k = skeys[koff + i];
+                    if (level == 0) atomicAdd(&sh.hist[(k - kmin) >> shift], 1u);
+                    else if (((k - kmin) >> shift) == bin0) atomicAdd(&sh.hist[(k - lo) >> sh1], 1u);
+                }
+            }
+            if (!one_batch) {
+                __syncthreads();
+                koff = fetch_keys(0);
+                wait_keys();
+            }
+            __syncthreads();
+            if (level == 0) SEL_TRACE(11);
+            if (warp == 0) find_bin_desc(sh.hist, kr, lane, &sh.st[1], &sh.st[9]);
+            __syncthreads();
+            const uint32_t bb = sh.st[1], above = sh.st[9];
+            lo += bb << sh1;
+            // a bin of few keys costs fewer extra candidates than a second pass costs time
+            if (level == 1 || sh1 == 0 || sh.hist[bb] <= kRefineMin) break;
+            bin0 = bb;
+            kr -= above;
+            sh1 = sh1 > 10 ? sh1 - 10 : 0;
+            for (uint32_t i = tid; i < uint32_t(kBins); i += kSThreads) sh.hist[i] = 0u;
+            __syncthreads();
+        }
+        SEL_TRACE(13);
+        thr = (e_int == 0xffffffffu || lo < 2ull * e_int) ? 0u : lo - 2u * e_int;
     }
-    if (warp < kSCons / 32 && (all || K > 1)) {
-        for (uint32_t b0 = warp * 32; b0 < ns; b0 += kSCons) {  // warp-uniform trip count
-            const uint32_t i = b0 + lane;
-            const bool cnd = i < ns && keys[i] >= thr;
-            const uint32_t m = __ballot_sync(0xffffffffu, cnd);
+    if (all || K > 1) {  // candidates {I_i >= thr}: per-thread counts, per-warp slots
+        for (uint32_t b0 = 0; b0 < nd; b0 += kFinKeys) {
+            if (b0 > 0) {
+                __syncthreads();
+                koff = fetch_keys(b0);
+                wait_keys();
+            }
+            const uint32_t nb = min(kFinKeys, nd - b0);
+            uint32_t cnt = 0;
+#pragma unroll 4
+            for (uint32_t i = tid; i < nb; i += kSThreads) cnt += skeys[koff + i] >= thr ? 1u : 0u;
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= uint32_t(o)) incl += v;
+            }
             uint32_t base = 0;
-            if (lane == 0 && m) base = atomicAdd(&sh.local_cnt, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (cnd) {
-                const uint32_t p = base + __popc(m & ((1u << lane) - 1u));
-                if (p < cand_cap) list[p] = i;
+            if (lane == 31 && incl) base = atomicAdd(&sh.local_cnt, incl);
+            uint32_t pos = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+            if (cnt) {
+#pragma unroll 1
+                for (uint32_t i = tid; i < nb; i += kSThreads) {
+                    if (skeys[koff + i] >= thr) {
+                        if (pos < cand_cap) list[pos] = b0 + i;
+                        ++pos;
+                    }
+                }
             }
         }
+    }
+    __syncthreads();  // candidate list complete
+    SEL_TRACE(8);
+    const uint32_t n = sh.local_cnt;
+#ifdef ABSP_ATTN_TRACE
+    if (tid == 0 && blockIdx.x < 4096) g_sel_trace[blockIdx.x * kSelTraceSlots + 14] = n;
+#endif
+    // exact scores of the candidates and of the trailing block (entry n), their pages
+    // prefetched into shared memory for the emit below
+    const uint32_t n_sc = n <= cand_cap ? n + (trailing ? 1u : 0u) : (trailing ? 1u : 0u);
+    const bool pg_pre = pages.page && n <= cand_cap && (n + 1) * ppb <= plan.pg_cap;
+    for (uint32_t j = tid; j < n_sc; j += kSThreads) {
+        const bool tr = n > cand_cap || j == n;  // the trailing block
+        const uint32_t i = tr ? N - 1 : list[j];
+        const uint32_t slot = tr ? n : j;
+        uint32_t wd[W];
+        load_row_global<W>(L.codes, du.seg + i, i, wd);
+        if (pg_pre || (tr && pages.page)) {
+#pragma unroll 1
+            for (uint32_t pp = 0; pp < ppb; ++pp) {
+                const uint32_t t0 = i * du.block + pp * L.P;
+                const uint32_t pg = t0 < du.n_tokens ? head_base + __ldg(pt + t0 / L.P) : 0u;
+                if (tr) sh.tpg[pp] = pg;
+                else cpg[slot * ppb + pp] = pg;
+            }
+        }
+        const float x = exact_row<W>(wd, tbl);
+        const unsigned long long comp = (uint64_t(order_key(x)) << 32) | uint32_t(~i);
+        if (tr) sh.ct = comp;
+        else cand[slot] = comp;
     }
     __syncthreads();
-    const uint32_t nl = sh.local_cnt;
-    const uint32_t leader_cnt = dsmem(&sh.cand_cnt, 0), leader_of = dsmem(&sh.overflow, 0);
-    if (nl > cand_cap) {
-        if (tid == 0) red_or_cluster(leader_of, 1u);
-    } else if (nl > 0) {
-        if (tid == 0) sh.st[2] = atom_add_cluster(leader_cnt, nl);
-        __syncthreads();
-        const uint32_t pos0 = sh.st[2];
-        if (pos0 + nl > cand_cap) {
-            if (tid == 0) red_or_cluster(leader_of, 1u);
-        } else {
-            for (uint32_t j = tid; j < nl; j += kSThreads) {
-                const uint32_t i = list[j];
-                uint32_t wd[W];
-                if (resident) {
-                    const unsigned char* src = ring + size_t(i / kSRows) * C::STAGEB + (i % kSRows) * C::ROWB;
-                    const uint32_t key = code_row_key(s0 + i, W);
-#pragma unroll
-                    for (int g = 0; g < W / 4; ++g) {
-                        const uint4 v = *reinterpret_cast<const uint4*>(src + ((g ^ key) << 4));
-                        wd[4 * g] = v.x;
-                        wd[4 * g + 1] = v.y;
-                        wd[4 * g + 2] = v.z;
-                        wd[4 * g + 3] = v.w;
-                    }
-                } else {
-                    load_row_global<W>(L.codes, du.seg + s0 + i, s0 + i, wd);
-                }
-                const float x = exact_row<W>(wd, tbl);
-                const unsigned long long comp = (uint64_t(order_key(x)) << 32) | uint32_t(~(s0 + i));
-                st_cluster_u64(dsmem(&cand[pos0 + j], 0), comp);
-            }
-        }
-    }
-    SEL_TRACE(8);
-    cluster_sync();  // #2: every composite has landed in the leader
     SEL_TRACE(9);
-    if (r != 0) return;
-
-    // ================================ leader ===================================
-    const unsigned long long ct = trailing ? (uint64_t(sh.st[3]) << 32) | uint32_t(~(N - 1)) : 0ull;
-    const uint32_t n = sh.cand_cnt;
+    const unsigned long long ct = trailing ? sh.ct : 0ull;
     const uint32_t K1 = trailing ? K - 1 : n;
-    SEL_TRACE(10);
-    if (trailing && (K > 1) && (sh.overflow || n < K1)) {  // mass ties: exact fallback
+    if (trailing && (K > 1) && (n > cand_cap || n < K1)) {  // mass ties: exact fallback
         exact_fallback<W>(L, du, sh, tbl, K, ct);
         publish_selection(L, du, u, sh.outs, K, blocks, stride, counts, pages, ready);
         SEL_TRACE(12);
@@ -713,29 +777,22 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     }
     // Order and publish in one pass: the rank of a candidate among the candidates is its
     // output position (composites are distinct); the trailing block goes after every
-    // winner above it. The thread that ranks a winner writes its block id and resolves
-    // its pages straight into the attention producer's page list.
+    // winner above it. The thread that ranks a winner writes its block id and its pages
+    // straight into the attention producer's page list.
     const uint32_t n_sel = trailing ? K : n;
-    const uint32_t ppb = du.block / L.P;
-    const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
-    const uint32_t head_base = du.head * uint32_t(L.pool_pages);
     const size_t pbase = pages.page ? size_t(pages.chunk_base[u]) * pages.ns : 0;
-    auto emit = [&](uint32_t p, uint32_t blk) {
+    // j: candidate index (pages in cpg), kNoPrefetch (page table), ~0u: the trailing block
+    auto emit = [&](uint32_t p, uint32_t blk, uint32_t j) {
         blocks[size_t(u) * stride + p] = blk;
         if (!pages.page) return;
-        if (trailing && blk == N - 1) {  // resolved at the start
-            for (uint32_t pp = 0; pp < ppb; ++pp) {
-                pages.page[pbase + size_t(p) * ppb + pp] = sh.tpg[pp];
-                pages.valid[pbase + size_t(p) * ppb + pp] = uint16_t(sh.tvl[pp]);
-            }
-            return;
-        }
+#pragma unroll 1
         for (uint32_t pp = 0; pp < ppb; ++pp) {
             const uint32_t t0 = blk * du.block + pp * L.P;
             uint32_t v = 0, page = 0;
             if (t0 < du.n_tokens) {
                 v = min(L.P, du.n_tokens - t0);
-                page = head_base + __ldg(pt + t0 / L.P);
+                page = j == ~0u ? sh.tpg[pp] : (pg_pre && j != kNoPrefetch) ? cpg[j * ppb + pp]
+                                                                            : head_base + __ldg(pt + t0 / L.P);
             }
             pages.page[pbase + size_t(p) * ppb + pp] = page;
             pages.valid[pbase + size_t(p) * ppb + pp] = uint16_t(v);
@@ -757,20 +814,20 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         for (uint32_t off = 1; off < tpc; off <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
         if (valid && part == 0 && rank < K1) {
             above = trailing && me > ct;
-            emit(rank + (trailing && ct > me ? 1u : 0u), ~uint32_t(me));
+            emit(rank + (trailing && ct > me ? 1u : 0u), ~uint32_t(me), j);
         }
     } else {  // large candidate sets (large budgets): sort, then emit by position
-        sort_desc(cand, n);
+        sort_desc(cand, n);  // positions change: pages are resolved from the page table
         for (uint32_t p = tid; p < K1; p += kSThreads) {
             const unsigned long long me = cand[p];
             if (trailing && me > ct) atomicAdd(&sh.nsel, 1u);
-            emit(p + (trailing && ct > me ? 1u : 0u), ~uint32_t(me));
+            emit(p + (trailing && ct > me ? 1u : 0u), ~uint32_t(me), kNoPrefetch);
         }
     }
-    SEL_TRACE(11);
+    SEL_TRACE(10);
     uint32_t n_above = __syncthreads_count(above);
     if (n > uint32_t(kSThreads)) n_above = sh.nsel;  // (set before the barrier above)
-    if (trailing && tid == 0) emit(n_above, N - 1);
+    if (trailing && tid == 0) emit(n_above, N - 1, ~0u);
     if (pages.page) {  // the rest of the unit's last attention chunk: empty slots
         const uint32_t E = kAttnChunkRows / du.block;
         const uint32_t slot_end = ((n_sel + E - 1) / E * E) * ppb;
@@ -796,61 +853,67 @@ bool select_fused_supported(const LayerView& L) {
     return L.bits == 4 && L.method == ABSP_CENTROID_MEAN && (L.D == 64 || L.D == 128) && L.G <= 8;
 }
 
-// Cluster size and shared-memory plan of a layer: enough CTAs per unit to cover the SMs
-// (cfg3 on 1 GPU: 128 units x 2; its 8-GPU shard: 16 units x 8), the key slice for the
-// largest unit at capacity, 4 ring stages when they fit (2 CTAs per SM if possible).
-SelectPlan plan_select(uint32_t units, uint32_t max_cap_blocks, uint32_t max_budget, uint32_t D, int num_sms) {
+size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_t pg_cap) {
+    return D == 64 ? SelLayout<64>(stages, cand_cap, pg_cap).total : SelLayout<128>(stages, cand_cap, pg_cap).total;
+}
+
+// Slices of a layout: the smallest slice size S (a multiple of 256 rows, at most 4096)
+// that keeps the layer within about two resident CTAs per SM (cfg3 on one GPU: S = 2304,
+// 320 slices; its 8-GPU shard: S = 512), the unit's candidate domain cut evenly into
+// ceil(nd / S) slices, in unit order. Ring stages: 4 when they fit (2 CTAs per SM).
+SelectPlan plan_select(const std::vector<UnitDesc>& desc, uint32_t max_budget, uint32_t D, int num_sms,
+                       std::vector<SliceDesc>* slices) {
     SelectPlan p{};
-    p.cluster = 1;
-    while (p.cluster < 8 && units * p.cluster < uint32_t(num_sms)) p.cluster <<= 1;
+    auto nd_of = [](const UnitDesc& d) { return d.n_blocks <= d.budget ? d.n_blocks : d.n_blocks - 1; };
+    auto count = [&](uint32_t S) {
+        uint64_t c = 0;
+        for (const UnitDesc& d : desc) c += std::max(1u, (nd_of(d) + S - 1) / S);
+        return c;
+    };
+    p.rows = kSliceMin;
+    while (p.rows < kSliceMax && count(p.rows) > uint64_t(2 * num_sms)) p.rows += kSliceMin;
     p.cand_cap = 512;  // a power of two (bitonic sort in place), >= K
     while (p.cand_cap < kCandCapMax && p.cand_cap < 4 * max_budget) p.cand_cap <<= 1;
-    p.slice_cap = (max_cap_blocks + p.cluster - 1) / p.cluster + 1;
+    p.pg_cap = 4096;
     for (p.stages = kSStages; p.stages > 2; --p.stages)
-        if (select_fused_smem(D, p.stages, p.slice_cap, p.cand_cap) <= 227 * 1024) break;
-    p.ok = select_fused_smem(D, p.stages, p.slice_cap, p.cand_cap) <= 227 * 1024;
+        if (select_fused_smem(D, p.stages, p.cand_cap, p.pg_cap) * 2 + 2048 <= 228 * 1024) break;
+    p.ok = select_fused_smem(D, p.stages, p.cand_cap, p.pg_cap) <= 227 * 1024;
+    if (slices) {
+        slices->clear();
+        for (uint32_t u = 0; u < desc.size(); ++u) {
+            const uint32_t n = std::max(1u, (nd_of(desc[u]) + p.rows - 1) / p.rows);
+            const uint32_t first = uint32_t(slices->size());
+            for (uint32_t r = 0; r < n; ++r) slices->push_back(SliceDesc{u, r, n, first});
+        }
+    }
+    p.n_slices = slices ? uint32_t(slices->size()) : uint32_t(count(p.rows));
     return p;
 }
 
-size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t slice_cap, uint32_t cand_cap) {
-    return D == 64 ? SelLayout<64>(stages, slice_cap, cand_cap).total : SelLayout<128>(stages, slice_cap, cand_cap).total;
+// Slices a unit can ever need (reservation at bind: every unit at capacity, S = 256).
+uint64_t select_slices_bound(const std::vector<UnitDesc>& desc) {
+    uint64_t c = 0;
+    for (const UnitDesc& d : desc) c += std::max<uint64_t>(1, (uint64_t(std::max(d.n_blocks, d.cap)) + kSliceMin - 1) / kSliceMin);
+    return c;
 }
 
 cudaError_t init_select_attributes() {
     cudaError_t e = cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, uint32_t* blocks,
-                                uint32_t stride, uint32_t* counts, const PageList& pages, uint32_t* ready,
-                                float* diag_approx, float* diag_err, cudaStream_t s, int* launches) {
-    const uint32_t cluster = plan.cluster;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(L.units * cluster);
-    cfg.blockDim = dim3(kSThreads);
-    cfg.dynamicSmemBytes = select_fused_smem(L.D, plan.stages, plan.slice_cap, plan.cand_cap);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = cluster;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
+cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, const SelectWork& work,
+                                uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
+                                uint32_t* ready, float* diag_approx, float* diag_err, cudaStream_t s, int* launches) {
+    const size_t smem = select_fused_smem(L.D, plan.stages, plan.cand_cap, plan.pg_cap);
     cudaError_t e;
     if (L.D == 64)
-        e = cudaLaunchKernelEx(&cfg, k_select<64>, L, q, plan.stages, plan.slice_cap, plan.cand_cap, blocks, stride,
-                               counts, pages, ready, diag_approx, diag_err);
+        e = launch_pdl(k_select<64>, dim3(plan.n_slices), dim3(kSThreads), smem, s, L, q, plan, work, blocks, stride,
+                       counts, pages, ready, diag_approx, diag_err);
     else
-        e = cudaLaunchKernelEx(&cfg, k_select<128>, L, q, plan.stages, plan.slice_cap, plan.cand_cap, blocks, stride,
-                               counts, pages, ready, diag_approx, diag_err);
+        e = launch_pdl(k_select<128>, dim3(plan.n_slices), dim3(kSThreads), smem, s, L, q, plan, work, blocks,
+                       stride, counts, pages, ready, diag_approx, diag_err);
     ++*launches;
     return e == cudaSuccess ? cudaGetLastError() : e;
 }

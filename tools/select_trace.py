@@ -45,29 +45,34 @@ with torch.cuda.stream(stream):
     with torch.cuda.graph(g, stream=stream):
         da.decode_step(0, q, out, stream)
 flush = torch.empty(1 << 28, dtype=torch.int8, device="cuda")
-names = ["start", "wait done", "cluster0", "params", "table+wts", "filter done", "bound", "cluster1",
-         "cands scored", "cluster2", "trailing", "ordered", "published"]
+names = ["start", "wait done", "fin: loaded", "params", "weights", "filter done", "keys out", "arrived",
+         "fin: cands", "fin: scored", "fin: ranked", "fin: hist", "published", "fin: thr"]
 pct = lambda a: " ".join(f"{x:7.2f}" for x in np.percentile(a, [0, 10, 50, 90, 100]))
+import os
+warm = os.environ.get("SEL_TRACE_WARM") == "1"  # no L2 flush: the previous replay's code and data stay
 for rep in range(2):
-    flush.fill_(rep)
+    if not warm:
+        flush.fill_(rep)
     torch.cuda.synchronize()
     g.replay()
     torch.cuda.synchronize()
-    st = np.zeros((2048, 16), np.uint64)
+    st = np.zeros((4096, 16), np.uint64)
     at = np.zeros((160, 256), np.uint64)
     _abi.check(_abi._lib.absp_debug_select_trace(st.ctypes.data, st.nbytes))
     _abi.check(_abi._lib.absp_debug_attn_trace(at.ctypes.data, at.nbytes))
     ncta = int((st[:, 0] > 0).sum())
     st = st[:ncta]
     t0 = st[:, 0].min()
-    print(f"rep {rep}: {ncta} select CTAs (us from the first start; pctl 0/10/50/90/100)")
-    for i, nm in enumerate(names):
+    print(f"rep {rep}{' (warm)' if warm else ''}: {ncta} select CTAs (us from the first start; pctl 0/10/50/90/100)")
+    for i in (0, 1, 3, 4, 5, 6, 7, 2, 11, 13, 8, 9, 10, 12):
+        nm = names[i]
         col = st[:, i]
-        col = col[col > 0]
+        col = col[col >= t0]  # stale stamps of earlier steps are older than this step's start
         if len(col):
             print(f"  {nm:14s} {pct((col.astype(np.float64) - t0) / 1e3)}  (n={len(col)})")
-    lead = st[:, 13][st[:, 12] > 0]
-    print("  candidates/unit", pct(lead & 0xffffffff), " overflow units", int(((lead >> 32) > 0).sum()))
+    fin = st[st[:, 12] >= t0]
+    if len(fin):
+        print("  candidates/unit", pct(fin[:, 14].astype(np.float64)))
     a0 = at[:, 0]
     live = a0 > 0
     if live.any():
