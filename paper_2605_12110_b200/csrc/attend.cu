@@ -125,7 +125,7 @@ struct StageMeta {
     __align__(16) uint16_t q[8 * 128];  // the chunk's unit's G query rows (bf16)
     uint32_t unit;
     uint32_t chunk;             // bit 31: some row of the chunk carries no token
-    uint8_t valid[kMaxSlots];   // valid rows per page slot (0..P; P <= 128)
+    __align__(4) uint8_t valid[kMaxSlots];   // valid rows per page slot (0..P; P <= 128)
 };
 
 template <int D>
@@ -253,9 +253,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
                 const uint32_t s = k * 32 + lane;
-                if (s < NS) mt.valid[s] = uint8_t(vl[k]);
                 bytes += __reduce_add_sync(0xffffffffu, vl[k] ? 2 * P * D * 2 : 0u);
                 invalid |= __ballot_sync(0xffffffffu, s < NS && vl[k] < P);
+                // valid[] is stored by lane 0, the thread whose arrive on `full` (release)
+                // publishes the stage: 4 slots per word, gathered by shuffles
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    uint32_t wv = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) wv |= __shfl_sync(0xffffffffu, vl[k], 4 * m + e) << (8 * e);
+                    if (lane == 0 && k * 32 + 4 * m < int(NS)) reinterpret_cast<uint32_t*>(mt.valid)[k * 8 + m] = wv;
+                }
             }
             if (lane == 0) {
                 mt.unit = u;
