@@ -268,6 +268,23 @@ absp_status absp_attention_recall(absp_ctx* ctx, uint32_t layer, const double* w
                                   const uint32_t* blocks, uint32_t blocks_stride, const uint32_t* counts,
                                   double* recall, void* stream);
 
+/* One calibration sample (the per-trace body of profile_sensitivity and
+ * transfer_check, calibrator.cpp:73-106 / :159-200) on the GPU, synchronous: the trace
+ * (keys / values fp32 [num_kv_heads][seq_len][head_dim], queries fp32
+ * [num_q_heads][head_dim], host memory, stored as bf16 like every input of this build)
+ * becomes a paged cache with sequential pages (cache_from_trace, workload.cpp:311-330);
+ * absp_full_attention gives the oracle weights; for every candidate block size a
+ * uniform assignment is built, quantized (cfg's QuantSpec), estimated and selected at
+ * cfg->token_budget, and its attention_recall written to recalls (fp64
+ * [num_kv_heads][num_candidates], RecallTable::recalls layout, calibrator.hpp:15-28;
+ * with GQA the mean over the G query heads of a KV head). With `assignment`
+ * (block size per KV head) its recall per KV head goes to assigned_recall.
+ * cfg->max_batch / max_seq_len / num_layers are ignored. The reference skips traces
+ * with seq_len <= token_budget; so does the host side of this build. */
+absp_status absp_profile_sample(int device, const absp_config* cfg, const float* keys, const float* values,
+                                const float* queries, uint64_t seq_len, const uint32_t* assignment,
+                                double* recalls, double* assigned_recall);
+
 /* Deterministic counter-based N(0,1)-like bf16 generator used by the benchmark
  * and tests (same bytes as oracle/synth.py): element i of stream s gets
  * splitmix64(seed + golden * (s * 2^40 + i + 1)) -> Irwin-Hall(4 x u16) -> fp32

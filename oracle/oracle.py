@@ -97,6 +97,14 @@ def ref() -> C.CDLL:
                                       C.c_void_p, C.POINTER(C.c_int)]
         L.ref_engine_store.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.POINTER(_sz)]
+        _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        L.ref_save_trace.argtypes = [C.c_char_p, _sz, _sz, _sz, C.c_uint64, _f32p, _f32p, _f32p]
+        L.ref_load_trace.argtypes = [C.c_char_p, _u64p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_profile_sensitivity.argtypes = [_sz, _sz, _sz, C.POINTER(_sz), _sz, _sz, C.c_int, C.c_int, C.c_int,
+                                              _sz, _sz, _f32p, _f32p, _f32p, _f64p]
+        L.ref_transfer_check.argtypes = [_sz, _sz, _sz, C.POINTER(_sz), _sz, _sz, C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(_sz), _sz, _sz, _f32p, _f32p, _f32p, _f64p]
+        L.ref_assign_block_sizes.argtypes = [_sz, C.POINTER(_sz), _sz, _f64p, C.c_double, C.POINTER(_sz)]
         L.ref_config_validate.argtypes = [_sz, _sz, _sz, C.POINTER(_sz), _sz, _sz, C.c_int]
         L.ref_generate_synthetic.argtypes = [_sz, _sz, _sz, C.POINTER(C.c_int), C.POINTER(_sz),
                                              C.POINTER(_sz), C.c_double, C.c_uint64, _sz, _f32p,
@@ -418,3 +426,60 @@ def ref_generate_synthetic(n, H, d, profiles, signal=8.0, seed=0, scatter_gap=64
     qs = np.zeros((H, d), np.float32)
     _rcheck(ref().ref_generate_synthetic(n, H, d, kinds, a, b, signal, seed, scatter_gap, keys, vals, qs))
     return keys, vals, qs
+
+
+# ---------------------------------------------------------------------------
+# Trace I/O and calibration of the unmodified reference (workload.cpp, calibrator.cpp)
+# ---------------------------------------------------------------------------
+def ref_save_trace(path, keys, values, queries, seed=0):
+    keys = np.ascontiguousarray(keys, np.float32)
+    H, n, d = keys.shape
+    _rcheck(ref().ref_save_trace(str(path).encode(), H, d, n, seed, keys,
+                                 np.ascontiguousarray(values, np.float32), np.ascontiguousarray(queries, np.float32)))
+
+
+def ref_load_trace(path):
+    """(keys [H][n][d], values, queries [H][d], seed) read by the reference's load_trace."""
+    dims = np.zeros(4, np.uint64)
+    _rcheck(ref().ref_load_trace(str(path).encode(), dims, None, None, None))
+    H, d, n, seed = (int(x) for x in dims)
+    k = np.zeros((H, n, d), np.float32)
+    v = np.zeros((H, n, d), np.float32)
+    q = np.zeros((H, d), np.float32)
+    _rcheck(ref().ref_load_trace(str(path).encode(), dims, k.ctypes.data, v.ctypes.data, q.ctypes.data))
+    return k, v, q, seed
+
+
+def _calib_args(H, d, P, cands, T, method, bits, mode):
+    return (H, d, P, (_sz * len(cands))(*cands), len(cands), T, method, bits, mode)
+
+
+def ref_profile_sensitivity(keys, values, queries, P, cands, T, method=0, bits=4, mode=1):
+    """keys/values [S][H][n][d], queries [S][H][d] -> recalls [H][len(cands)]."""
+    keys = np.ascontiguousarray(keys, np.float32)
+    S, H, n, d = keys.shape
+    out = np.zeros((H, len(cands)), np.float64)
+    _rcheck(ref().ref_profile_sensitivity(*_calib_args(H, d, P, cands, T, method, bits, mode), S, n, keys,
+                                          np.ascontiguousarray(values, np.float32),
+                                          np.ascontiguousarray(queries, np.float32), out))
+    return out
+
+
+def ref_transfer_check(block_sizes, keys, values, queries, P, cands, T, method=0, bits=4, mode=1):
+    """-> dict(adaptive_recall, delta, avg_block_size, matched_candidate, uniform_recalls)."""
+    keys = np.ascontiguousarray(keys, np.float32)
+    S, H, n, d = keys.shape
+    out = np.zeros(4 + len(cands), np.float64)
+    _rcheck(ref().ref_transfer_check(*_calib_args(H, d, P, cands, T, method, bits, mode),
+                                     (_sz * H)(*block_sizes), S, n, keys, np.ascontiguousarray(values, np.float32),
+                                     np.ascontiguousarray(queries, np.float32), out))
+    return dict(adaptive_recall=out[0], delta=out[1], avg_block_size=out[2], matched_candidate=int(out[3]),
+                uniform_recalls=list(out[4:]))
+
+
+def ref_assign_block_sizes(recalls, cands, tau):
+    recalls = np.ascontiguousarray(recalls, np.float64)
+    H = recalls.shape[0]
+    out = (_sz * H)()
+    _rcheck(ref().ref_assign_block_sizes(H, (_sz * len(cands))(*cands), len(cands), recalls, tau, out))
+    return [int(x) for x in out]

@@ -13,6 +13,8 @@
 //   sparse_attention          engine.hpp:79-80
 //   full_attention_oracle     engine.hpp:86
 //   DecodeEngine              engine.hpp:99-129
+//   save_trace / load_trace   workload.hpp:70-71
+//   profile_sensitivity, transfer_check, assign_block_sizes   calibrator.hpp:52-76
 //
 // One handle = one sequence (the reference has no batch dimension,
 // kv_cache.hpp:26-67). Batch and GQA are layered on top in Python exactly as
@@ -27,6 +29,7 @@
 #include <string>
 #include <vector>
 
+#include "absparse/calibrator.hpp"
 #include "absparse/centroids.hpp"
 #include "absparse/config.hpp"
 #include "absparse/engine.hpp"
@@ -372,6 +375,109 @@ int ref_generate_synthetic(size_t n, size_t H, size_t d, const int* kinds, const
         std::memcpy(keys, t.keys.data(), t.keys.size() * sizeof(float));
         std::memcpy(values, t.values.data(), t.values.size() * sizeof(float));
         std::memcpy(queries, t.queries.data(), t.queries.size() * sizeof(float));
+    });
+}
+
+// ---- trace I/O and calibration (workload.cpp:260-309, calibrator.cpp) ----------
+int ref_save_trace(const char* path, size_t H, size_t d, size_t n, uint64_t seed, const float* keys,
+                   const float* values, const float* queries) {
+    return guard([&] {
+        Trace t;
+        t.num_heads = H;
+        t.head_dim = d;
+        t.seq_len = n;
+        t.seed = seed;
+        t.keys.assign(keys, keys + H * n * d);
+        t.values.assign(values, values + H * n * d);
+        t.queries.assign(queries, queries + H * d);
+        save_trace(t, path);
+    });
+}
+
+// dims: H, d, n, seed (as u64 x4); arrays sized by the caller after a first call with
+// keys == nullptr (dims only).
+int ref_load_trace(const char* path, uint64_t* dims, float* keys, float* values, float* queries) {
+    return guard([&] {
+        const Trace t = load_trace(path);
+        dims[0] = t.num_heads;
+        dims[1] = t.head_dim;
+        dims[2] = t.seq_len;
+        dims[3] = t.seed;
+        if (!keys) return;
+        std::memcpy(keys, t.keys.data(), t.keys.size() * 4);
+        std::memcpy(values, t.values.data(), t.values.size() * 4);
+        std::memcpy(queries, t.queries.data(), t.queries.size() * 4);
+    });
+}
+
+namespace {
+EngineConfig calib_config(size_t H, size_t d, size_t P, const size_t* cands, size_t nc, size_t T, int method,
+                          int bits, int mode) {
+    EngineConfig c;
+    c.num_heads = H;
+    c.head_dim = d;
+    c.page_size = P;
+    c.candidate_block_sizes.assign(cands, cands + nc);
+    c.token_budget = T;
+    c.centroid_method = method == 0 ? CentroidMethod::kMean : CentroidMethod::kMaxMin;
+    c.quant = make_spec(bits, mode);
+    return c;
+}
+// samples back to back: keys/values [S][H][n][d], queries [S][H][d]
+TraceProvider calib_provider(size_t H, size_t d, size_t n, const float* keys, const float* values,
+                             const float* queries) {
+    return [=](size_t i) {
+        Trace t;
+        t.num_heads = H;
+        t.head_dim = d;
+        t.seq_len = n;
+        t.seed = i;
+        const size_t per = H * n * d;
+        t.keys.assign(keys + i * per, keys + (i + 1) * per);
+        t.values.assign(values + i * per, values + (i + 1) * per);
+        t.queries.assign(queries + i * H * d, queries + (i + 1) * H * d);
+        return t;
+    };
+}
+}  // namespace
+
+// recalls: [H][nc]
+int ref_profile_sensitivity(size_t H, size_t d, size_t P, const size_t* cands, size_t nc, size_t T, int method,
+                            int bits, int mode, size_t samples, size_t n, const float* keys, const float* values,
+                            const float* queries, double* recalls) {
+    return guard([&] {
+        const EngineConfig c = calib_config(H, d, P, cands, nc, T, method, bits, mode);
+        const RecallTable t = profile_sensitivity(calib_provider(H, d, n, keys, values, queries), samples, c);
+        std::memcpy(recalls, t.recalls.data(), t.recalls.size() * sizeof(double));
+    });
+}
+
+// out: adaptive_recall, delta, avg_block_size, matched_candidate, uniform_recalls[nc]
+int ref_transfer_check(size_t H, size_t d, size_t P, const size_t* cands, size_t nc, size_t T, int method,
+                       int bits, int mode, const size_t* block_sizes, size_t samples, size_t n, const float* keys,
+                       const float* values, const float* queries, double* out) {
+    return guard([&] {
+        const EngineConfig c = calib_config(H, d, P, cands, nc, T, method, bits, mode);
+        BlockAssignment a;
+        a.block_sizes.assign(block_sizes, block_sizes + H);
+        const TransferReport r = transfer_check(a, calib_provider(H, d, n, keys, values, queries), samples, c);
+        out[0] = r.adaptive_recall;
+        out[1] = r.delta;
+        out[2] = r.avg_block_size;
+        out[3] = double(r.matched_candidate);
+        for (size_t i = 0; i < nc; ++i) out[4 + i] = r.uniform_recalls[i];
+    });
+}
+
+int ref_assign_block_sizes(size_t H, const size_t* cands, size_t nc, const double* recalls, double tau,
+                           size_t* out) {
+    return guard([&] {
+        RecallTable t;
+        t.num_heads = H;
+        t.candidates.assign(cands, cands + nc);
+        t.recalls.assign(recalls, recalls + H * nc);
+        const BlockAssignment a = assign_block_sizes(t, tau);
+        for (size_t h = 0; h < H; ++h) out[h] = a.block_sizes[h];
     });
 }
 

@@ -31,7 +31,7 @@ EXPORTED = [
     "absp_get_layer_info", "absp_download_store", "absp_download_scores", "absp_download_selection", "absp_download_filter_scores",
     "absp_fill_synthetic_bf16", "absp_launch_count", "absp_attend_validate", "absp_layout_version", "absp_set_filter_diagnostics",
     "absp_engine_create", "absp_engine_destroy", "absp_engine_prefill", "absp_engine_step", "absp_engine_info",
-    "absp_full_attention", "absp_attention_recall",
+    "absp_full_attention", "absp_attention_recall", "absp_profile_sample",
 ]
 
 
@@ -142,6 +142,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
     L.absp_engine_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u32), C.POINTER(vp)]
     L.absp_full_attention.argtypes = [vp, u32, vp, vp, vp, u64, vp]
     L.absp_attention_recall.argtypes = [vp, u32, vp, u64, vp, u32, vp, vp, vp]
+    L.absp_profile_sample.argtypes = [C.c_int, C.POINTER(Config), vp, vp, vp, u64, u32p, vp, vp]
     L.absp_launch_count.argtypes = [vp]
     L.absp_launch_count.restype = u64
     for name in EXPORTED:

@@ -20,7 +20,7 @@ LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libabsp.so"
 OBJDIR = ROOT / "build" / "obj"
 
-SOURCES = ["api.cu", "engine.cu", "build_store.cu", "score.cu", "topk.cu", "select.cu", "attend.cu", "dense.cu", "synth.cu"]
+SOURCES = ["api.cu", "engine.cu", "build_store.cu", "score.cu", "topk.cu", "select.cu", "attend.cu", "dense.cu", "calibrate.cu", "synth.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
