@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Pa
         if (not force and obj.exists()
                 and obj.stat().st_mtime >= max(newest_header, (CSRC / src).stat().st_mtime)):
             continue
-        cmd = [nvcc(), *ARCH, *FLAGS, *(["-DABSP_ATTN_TRACE"] if trace else []), "-I", str(ROOT / "include"),
+        cmd = [nvcc(), *ARCH, *FLAGS, *(["-DABSP_ATTN_TRACE"] if trace else []),
+               *os.environ.get("ABSP_EXTRA_NVCC", "").split(), "-I", str(ROOT / "include"),
                "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
