@@ -412,12 +412,10 @@ def run_absp(args, w, rank, world, local):
         with torch.cuda.graph(ga, stream=stream):
             da.attend_selected(l, layers[l]["q"], layers[l]["out"], stream)
         att_graphs.append(ga)
-        sel_blocks = torch.empty(B, Hl, stride, dtype=torch.int32, device=dev)
-        sel_counts = torch.empty(B, Hl, dtype=torch.int32, device=dev)
-        gs = torch.cuda.CUDAGraph()
+        gs = torch.cuda.CUDAGraph()  # the step's own selection (fused kernel), no attention
         with torch.cuda.graph(gs, stream=stream):
-            da.select(l, layers[l]["q"], sel_blocks, sel_counts, stream)
-        sel_graphs.append((gs, sel_blocks, sel_counts))
+            da.select_step(l, layers[l]["q"], stream)
+        sel_graphs.append((gs, None, None))
 
     def sync_all():
         torch.cuda.synchronize()

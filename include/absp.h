@@ -195,6 +195,11 @@ uint64_t absp_layout_version(absp_ctx* ctx, uint32_t layer);
 absp_status absp_attend_selected(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
                                  void* stream);
 
+/* The selection half of absp_decode_step into the layer's own buffers (the fused
+ * selection kernel; blocks / counts / page list), without the attention: pair with
+ * absp_attend_selected, e.g. to time or stream the two halves separately. */
+absp_status absp_select_step(absp_ctx* ctx, uint32_t layer, const void* q, void* stream);
+
 /* select + attend using context-owned selection buffers (the per-step hot path). */
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
                              void* stream);

@@ -31,7 +31,7 @@ EXPORTED = [
     "absp_get_layer_info", "absp_download_store", "absp_download_scores", "absp_download_selection", "absp_download_filter_scores",
     "absp_fill_synthetic_bf16", "absp_launch_count", "absp_attend_validate", "absp_layout_version", "absp_set_filter_diagnostics",
     "absp_engine_create", "absp_engine_destroy", "absp_engine_prefill", "absp_engine_step", "absp_engine_info",
-    "absp_full_attention", "absp_attention_recall", "absp_profile_sample",
+    "absp_full_attention", "absp_attention_recall", "absp_profile_sample", "absp_select_step",
 ]
 
 
@@ -123,6 +123,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
     L.absp_attend.argtypes = [vp, u32, vp, vp, u32, vp, vp, vp]
     L.absp_attend_selected.argtypes = [vp, u32, vp, vp, vp]
     L.absp_decode_step.argtypes = [vp, u32, vp, vp, vp]
+    L.absp_select_step.argtypes = [vp, u32, vp, vp]
     L.absp_decode_step_host.argtypes = [vp, u32, vp, vp, vp]
     L.absp_last_selection.argtypes = [vp, u32, C.POINTER(vp), u32p, C.POINTER(vp)]
     L.absp_get_layer_info.argtypes = [vp, u32, C.POINTER(LayerInfo)]

@@ -298,6 +298,10 @@ class DecodeAttention:
         """Attention over the layer's most recent selection (second half of decode_step)."""
         check(self._lib.absp_attend_selected(self._ctx, layer, _ptr(q), _ptr(out), _stream(stream)))
 
+    def select_step(self, layer: int, q, stream=None) -> None:
+        """The decode step's selection alone (layer-owned buffers; then attend_selected)."""
+        check(self._lib.absp_select_step(self._ctx, layer, _ptr(q), _stream(stream)))
+
     def decode_step(self, layer: int, q, out, stream=None) -> None:
         check(self._lib.absp_decode_step(self._ctx, layer, _ptr(q), _ptr(out), _stream(stream)))
 

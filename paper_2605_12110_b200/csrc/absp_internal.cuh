@@ -203,7 +203,10 @@ size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_
 cudaError_t init_select_attributes();  // per device, once
 cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, const SelectWork& work,
                                 uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                                uint32_t* ready, float* diag_approx, float* diag_err, cudaStream_t s, int* launches);
+                                uint32_t* ready, float* diag_approx, float* diag_err, uint16_t* q_copy, cudaStream_t s,
+                                int* launches);
+// q_copy (else null): q is read from (device-mapped pinned) host memory; each unit's
+// finalizing CTA copies the unit's G query rows to q_copy (device) for the attention.
 cudaError_t init_attend_attributes();  // per device, once
 // Dense fp64 decode attention with weights (dense.cu; full_attention_oracle,
 // engine.cpp:357-403) and attention_recall (calibrator.cpp:48-71).

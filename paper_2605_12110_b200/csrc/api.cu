@@ -244,6 +244,7 @@ struct Layer {
     const void* host_q = nullptr;
     float* host_out = nullptr;
     bool out_direct = false;  // the graph's attention writes host_out itself (mapped pinned memory)
+    bool q_direct = false;    // the graph's selection reads host_q itself (mapped pinned memory)
     int host_launches = 0;
     void drop_host_graph() {
         if (host_exec) cudaGraphExecDestroy(host_exec);
@@ -253,6 +254,7 @@ struct Layer {
         host_q = nullptr;
         host_out = nullptr;
         out_direct = false;
+        q_direct = false;
         h2d_node = d2h_node = nullptr;
     }
 
@@ -1003,6 +1005,45 @@ uint64_t absp_layout_version(absp_ctx* ctx, uint32_t layer) {
     return ctx->layers[layer].layout_version;
 }
 
+// The decode step's selection into the layer's own buffers: the fused kernel (or the
+// exact scorer + top-k), resolving the page list; `ready` raises the per-unit flags the
+// attention producer starts on (decode step only: its merges re-arm them).
+static bool fused_step_select(absp_ctx* ctx, Layer* l) {
+    return !ctx->exact_select && select_fused_supported(view_of(ctx, *l)) && l->sel_plan.ok;
+}
+
+static absp_status step_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t* ready, cudaStream_t s,
+                               uint16_t* q_copy = nullptr) {
+    const LayerView v = view_of(ctx, *l);
+    if (!ctx->exact_select && select_fused_supported(v) && l->sel_plan.ok) {
+        // balanced slices: integer tensor-core filter, exact refine, top-k and page resolution
+        int n = 0;
+        const SelectWork sw{l->sel_slices.p, l->sel_slot.p, l->sel_arrive.p, l->sel_keys.p};
+        cudaError_t e = launch_select_fused(v, static_cast<const uint16_t*>(q), l->sel_plan, sw, l->sel_blocks.p,
+                                            l->sel_stride, l->sel_counts.p, l->step_work.pages(), ready,
+                                            l->filter_diag ? l->approx.p : nullptr,
+                                            l->filter_diag ? l->unit_err.p : nullptr, q_copy, s, &n);
+        ctx->launches += n;
+        if (e != cudaSuccess) return cuda_fail(e, "select kernel");
+    } else {
+        if (q_copy) return fail(ABSP_EINVAL, "decode step: host-resident q needs the fused selection");
+        absp_status st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, ready, s);
+        if (st != ABSP_OK) return st;
+    }
+    l->selected = true;
+    return ABSP_OK;
+}
+
+absp_status absp_select_step(absp_ctx* ctx, uint32_t layer, const void* q, void* stream) {
+    Layer* l;
+    absp_status st = get_layer(ctx, layer, &l);
+    if (st != ABSP_OK) return st;
+    if (!l->built) return fail(ABSP_ESTATE, "select_step: call absp_build_store first");
+    if (!q) return fail(ABSP_EINVAL, "select_step: null pointer");
+    DeviceGuard dg(ctx->device);
+    return step_select(ctx, l, q, nullptr, cudaStream_t(stream));
+}
+
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
                              void* stream) {
     Layer* l;
@@ -1012,22 +1053,8 @@ absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float
     if (!q || !out) return fail(ABSP_EINVAL, "decode_step: null pointer");
     DeviceGuard dg(ctx->device);
     const cudaStream_t s = cudaStream_t(stream);
-    const LayerView v = view_of(ctx, *l);
-    if (!ctx->exact_select && select_fused_supported(v) && l->sel_plan.ok) {
-        // fused filter + exact refine + top-k + page resolution, one cluster per unit
-        int n = 0;
-        const SelectWork sw{l->sel_slices.p, l->sel_slot.p, l->sel_arrive.p, l->sel_keys.p};
-        cudaError_t e = launch_select_fused(v, static_cast<const uint16_t*>(q), l->sel_plan, sw, l->sel_blocks.p,
-                                            l->sel_stride, l->sel_counts.p, l->step_work.pages(), l->ready.p,
-                                            l->filter_diag ? l->approx.p : nullptr,
-                                            l->filter_diag ? l->unit_err.p : nullptr, s, &n);
-        ctx->launches += n;
-        if (e != cudaSuccess) return cuda_fail(e, "select kernel");
-    } else {
-        st = do_select(ctx, l, q, l->sel_blocks.p, l->sel_stride, l->sel_counts.p, l->ready.p, s);
-        if (st != ABSP_OK) return st;
-    }
-    l->selected = true;
+    st = step_select(ctx, l, q, l->ready.p, s);
+    if (st != ABSP_OK) return st;
     return do_attend_step(ctx, l, q, out, l->ready.p, s);
 }
 
@@ -1046,9 +1073,23 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
     const bool direct = cudaPointerGetAttributes(&pa, out_host) == cudaSuccess &&
                         pa.type == cudaMemoryTypeHost && pa.devicePointer == out_host;
     cudaGetLastError();
+    // Likewise a device-addressable pinned q: the selection kernel reads it over PCIe
+    // (one TMA copy of a unit's G rows per slice) and its finalizing CTAs leave each
+    // unit's rows in stage_q for the attention, so there is no copy before the step.
+    const bool q_direct = fused_step_select(ctx, l) && cudaPointerGetAttributes(&pa, q_host) == cudaSuccess &&
+                          pa.type == cudaMemoryTypeHost && pa.devicePointer == q_host;
+    cudaGetLastError();
     cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     absp_status st = ABSP_OK;
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && q_direct) {
+        float* o = direct ? out_host : l->stage_out.p;
+        st = step_select(ctx, l, q_host, l->ready.p, cap, l->stage_q.p);
+        if (st == ABSP_OK) st = do_attend_step(ctx, l, l->stage_q.p, o, l->ready.p, cap);
+        if (st == ABSP_OK && !direct)
+            e = cudaMemcpyAsync(out_host, l->stage_out.p, nq * sizeof(float), cudaMemcpyDeviceToHost, cap);
+        const cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+        if (e == cudaSuccess) e = e2;
+    } else if (e == cudaSuccess) {
         e = cudaMemcpyAsync(l->stage_q.p, q_host, nq * sizeof(uint16_t), cudaMemcpyHostToDevice, cap);
         if (e == cudaSuccess) st = absp_decode_step(ctx, layer, l->stage_q.p, direct ? out_host : l->stage_out.p, cap);
         if (e == cudaSuccess && st == ABSP_OK && !direct)
@@ -1072,7 +1113,7 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
             if (p.kind == cudaMemcpyHostToDevice) l->h2d_node = nodes[i];
             else if (p.kind == cudaMemcpyDeviceToHost) l->d2h_node = nodes[i];
         }
-        if (e == cudaSuccess && (!l->h2d_node || (!direct && !l->d2h_node))) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess && ((!q_direct && !l->h2d_node) || (!direct && !l->d2h_node))) e = cudaErrorInvalidValue;
         if (e == cudaSuccess) e = cudaGraphInstantiate(&l->host_exec, graph, 0);
     }
     cudaStreamDestroy(cap);
@@ -1090,6 +1131,7 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
     l->host_q = q_host;
     l->host_out = out_host;
     l->out_direct = direct;
+    l->q_direct = q_direct;
     return ABSP_OK;
 }
 
@@ -1108,7 +1150,8 @@ absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_h
     const cudaStream_t s = cudaStream_t(stream);
     if (!l->host_exec && capture_host_step(ctx, layer, l, q_host, out_host, nq) != ABSP_OK)
         l->drop_host_graph();
-    if (l->host_exec && l->out_direct && out_host != l->host_out) {  // the output is a kernel argument
+    if (l->host_exec && ((l->out_direct && out_host != l->host_out) || (l->q_direct && q_host != l->host_q))) {
+        // a host buffer the graph's kernels address directly changed: re-capture
         l->drop_host_graph();
         if (capture_host_step(ctx, layer, l, q_host, out_host, nq) != ABSP_OK) l->drop_host_graph();
     }
@@ -1116,8 +1159,10 @@ absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_h
     if (graph_ok && (q_host != l->host_q || out_host != l->host_out)) {
         // re-point the copy nodes; buffers the graph cannot take (e.g. pageable memory
         // after pinned) run this call eagerly and keep the graph as it is
-        cudaError_t e = cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, q_host,
-                                                           nq * sizeof(uint16_t), cudaMemcpyHostToDevice);
+        cudaError_t e = l->q_direct ? cudaSuccess
+                                    : cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p,
+                                                                         q_host, nq * sizeof(uint16_t),
+                                                                         cudaMemcpyHostToDevice);
         if (e == cudaSuccess && !l->out_direct)
             e = cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, out_host, l->stage_out.p,
                                                    nq * sizeof(float), cudaMemcpyDeviceToHost);
@@ -1127,8 +1172,9 @@ absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_h
         } else {
             cudaGetLastError();
             // the nodes may be half re-pointed: restore them for the next call
-            if (cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, l->host_q,
-                                                   nq * sizeof(uint16_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+            if ((!l->q_direct &&
+                 cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->h2d_node, l->stage_q.p, l->host_q,
+                                                    nq * sizeof(uint16_t), cudaMemcpyHostToDevice) != cudaSuccess) ||
                 (!l->out_direct &&
                  cudaGraphExecMemcpyNodeSetParams1D(l->host_exec, l->d2h_node, l->host_out, l->stage_out.p,
                                                     nq * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess)) {

@@ -222,6 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             if (ready && f.u != pu) {  // decode step: the unit's page list must be published
                 pu = f.u;
                 while (ld_acquire(ready + pu) == 0u) __nanosleep(32);
+                // the unit's q rows may have been written by the selection with generic
+                // stores (host-resident q, select.cu q_copy): order them before our TMA reads
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
             }
             const size_t base = size_t(w) * NS;
 #pragma unroll
@@ -259,10 +262,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                 // publishes the stage: 4 slots per word, gathered by shuffles
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
+                    if (k * 32 + 4 * m >= int(NS)) break;  // warp-uniform
                     uint32_t wv = 0;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) wv |= __shfl_sync(0xffffffffu, vl[k], 4 * m + e) << (8 * e);
-                    if (lane == 0 && k * 32 + 4 * m < int(NS)) reinterpret_cast<uint32_t*>(mt.valid)[k * 8 + m] = wv;
+                    if (lane == 0) reinterpret_cast<uint32_t*>(mt.valid)[k * 8 + m] = wv;
                 }
             }
             if (lane == 0) {

@@ -346,7 +346,8 @@ template <int D>
 __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint16_t* __restrict__ q, SelectPlan plan,
                                                        SelectWork sw, uint32_t* blocks, uint32_t stride,
                                                        uint32_t* counts, PageList pages, uint32_t* ready,
-                                                       float* diag_approx, float* diag_err) {
+                                                       float* diag_approx, float* diag_err,
+                                                       uint16_t* __restrict__ q_copy) {
     using C = SelCfg<D>;
     constexpr int W = C::W, NG = D / 32;  // code words per row, 16-byte groups (32 channels) per row
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -630,6 +631,9 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         ++kphase;
     };
     uint32_t koff = fetch_keys(0);
+    if (q_copy)  // q read from host memory: the attention gets the unit's rows in device memory
+        for (uint32_t i = tid; i < G * D / 8; i += kSThreads)
+            reinterpret_cast<uint4*>(q_copy + size_t(u) * G * D)[i] = reinterpret_cast<const uint4*>(qrows)[i];
     if (warp == kSWarps - 1) {  // the unit's key range: min / max over its slices
         uint32_t mn = 0xffffffffu, mx = 0u;
         for (uint32_t i = lane; i < Cn; i += 32) {
@@ -905,15 +909,16 @@ cudaError_t init_select_attributes() {
 
 cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, const SelectWork& work,
                                 uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
-                                uint32_t* ready, float* diag_approx, float* diag_err, cudaStream_t s, int* launches) {
+                                uint32_t* ready, float* diag_approx, float* diag_err, uint16_t* q_copy, cudaStream_t s,
+                                int* launches) {
     const size_t smem = select_fused_smem(L.D, plan.stages, plan.cand_cap, plan.pg_cap);
     cudaError_t e;
     if (L.D == 64)
         e = launch_pdl(k_select<64>, dim3(plan.n_slices), dim3(kSThreads), smem, s, L, q, plan, work, blocks, stride,
-                       counts, pages, ready, diag_approx, diag_err);
+                       counts, pages, ready, diag_approx, diag_err, q_copy);
     else
         e = launch_pdl(k_select<128>, dim3(plan.n_slices), dim3(kSThreads), smem, s, L, q, plan, work, blocks,
-                       stride, counts, pages, ready, diag_approx, diag_err);
+                       stride, counts, pages, ready, diag_approx, diag_err, q_copy);
     ++*launches;
     return e == cudaSuccess ? cudaGetLastError() : e;
 }

@@ -307,6 +307,18 @@ def test_decode_step_host_matches_device(cuda):
     out_host.zero_()
     gl.da.decode_step_host(0, q_host, out_host)
     assert np.array_equal(out_host.numpy(), dev)
+    # mixed: pinned q (read by the selection kernel itself) with pageable output, and
+    # pageable q with pinned output; then several steps in a row on the same graph
+    out4 = torch.zeros(dev.shape, dtype=torch.float32)
+    gl.da.decode_step_host(0, q2, out4)
+    assert np.array_equal(out4.numpy(), dev)
+    out_host.zero_()
+    gl.da.decode_step_host(0, torch.from_numpy(layer.q.view(np.int16).copy()), out_host)
+    assert np.array_equal(out_host.numpy(), dev)
+    for _ in range(3):
+        out_host.zero_()
+        gl.da.decode_step_host(0, q_host, out_host)
+        assert np.array_equal(out_host.numpy(), dev)
 
 
 def test_synthetic_generator_matches_host_twin(cuda):
