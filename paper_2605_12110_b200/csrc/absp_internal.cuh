@@ -192,14 +192,14 @@ struct SelectPlan {
 };
 struct SelectWork {
     const SliceDesc* slices;  // [n_slices], unit order
-    uint32_t* slot;           // [2 n_slices] per-slice key range (min, max)
+    uint32_t* slot;           // [4 n_slices] per-slice key range (min, max), bound t_r
     uint32_t* arrive;         // [units] slices done this step (zero between steps)
     uint32_t* keys;           // [store segment] integer filter keys
 };
 SelectPlan plan_select(const std::vector<UnitDesc>& desc, uint32_t max_budget, uint32_t D, int num_sms,
                        std::vector<SliceDesc>* slices);
 uint64_t select_slices_bound(const std::vector<UnitDesc>& desc);
-size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_t pg_cap);
+size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_t pg_cap, uint32_t rows);
 cudaError_t init_select_attributes();  // per device, once
 cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const SelectPlan& plan, const SelectWork& work,
                                 uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,

@@ -544,7 +544,7 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
     {
         const uint64_t bound = std::max<uint64_t>(select_slices_bound(l->desc), slices.size());
         ABSP_CUDA(l->sel_slices.ensure(bound));
-        ABSP_CUDA(l->sel_slot.ensure(2 * bound));
+        ABSP_CUDA(l->sel_slot.ensure(4 * bound));
         ABSP_CUDA(l->sel_arrive.ensure(units));
         ABSP_CUDA(l->sel_keys.ensure(l->total_cap + 8));  // + the TMA batches' 16-byte round-up
         if (!async) ABSP_CUDA(cudaMemset(l->sel_arrive.p, 0, units * 4));

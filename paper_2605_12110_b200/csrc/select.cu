@@ -110,6 +110,12 @@ struct SelHead {
     uint32_t cap;
 };
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cons_sync() {  // named barrier 1: the consumer warps
     asm volatile("bar.sync 1, %0;\n" ::"n"(kSCons) : "memory");
 }
@@ -322,20 +328,91 @@ __device__ __forceinline__ void find_bin_desc(const uint32_t* hist, uint32_t kr,
     }
 }
 
+// Bitonic sort (descending) of n <= 1024 composites a[0, 1024), zero-padded, by the 8
+// consumer warps (4 elements per lane in registers: element warp*128 + 32 r + lane):
+// distances 32 and 64 inside a thread, below 32 by shuffles, 128 and up through shared
+// memory (6 of the 55 stages). The producer warp only joins the barriers.
+__device__ void sort1024_desc(unsigned long long* a, uint32_t n) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint32_t i = n + tid; i < 1024u; i += blockDim.x) a[i] = 0ull;
+    __syncthreads();
+    const bool act = warp < 8;
+    const uint32_t base = warp * 128 + lane;
+    unsigned long long v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[r] = act ? a[base + 32 * r] : 0ull;
+    for (uint32_t k = 2; k <= 1024u; k <<= 1) {
+        uint32_t j = k >> 1;
+        if (j >= 128) {  // cross-warp distances through shared memory
+            if (act) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) a[base + 32 * r] = v[r];
+            }
+            __syncthreads();
+            for (; j >= 128; j >>= 1) {
+                for (uint32_t i = tid; i < 1024u; i += blockDim.x) {
+                    const uint32_t ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long x = a[i], y = a[ixj];
+                        if (((i & k) == 0) ? (x < y) : (x > y)) {
+                            a[i] = y;
+                            a[ixj] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if (act) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[r] = a[base + 32 * r];
+            }
+        }
+        if (!act) continue;
+        for (; j >= 32; j >>= 1) {  // registers r and r | j/32 of this thread
+            const int rr = int(j >> 5);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (r & rr) continue;
+                const bool desc = ((base + 32 * r) & k) == 0;
+                const unsigned long long x = v[r], y = v[r | rr];
+                const unsigned long long hi = x > y ? x : y, lo = x > y ? y : x;
+                v[r] = desc ? hi : lo;
+                v[r | rr] = desc ? lo : hi;
+            }
+        }
+        for (; j > 0; j >>= 1) {  // lanes ^ j, same register
+            const bool lower = (lane & j) == 0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                const bool desc = ((base + 32 * r) & k) == 0;
+                v[r] = (lower == desc) ? (v[r] > o ? v[r] : o) : (v[r] > o ? o : v[r]);
+            }
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[base + 32 * r] = v[r];
+    }
+    __syncthreads();
+}
+
 // Shared-memory layout (host and device): ring [stages][rows][row bytes] (in the
 // finalize: the candidate composites cand [cand_cap] u64, list / outs [cand_cap] u32, the
-// candidates' prefetched pages cpg [pg_cap] u32 and a batch of the unit's keys) | product
-// table | q rows | scales, zps | SelHead.
+// candidates' prefetched pages cpg [pg_cap] u32 and a batch of the unit's keys) | the
+// slice's keys [rows] (units of several key batches) | product table | q rows | scales,
+// zps | SelHead.
 template <int D>
 struct SelLayout {
-    size_t cand, list, cpg, fkeys, tbl, prm, head, total;
-    __host__ __device__ SelLayout(uint32_t stages, uint32_t cand_cap, uint32_t pg_cap) {
+    size_t cand, list, cpg, fkeys, slk, tbl, prm, head, total;
+    __host__ __device__ SelLayout(uint32_t stages, uint32_t cand_cap, uint32_t pg_cap, uint32_t rows) {
         cand = 0;
         list = size_t(cand_cap) * 8;
         cpg = list + size_t(cand_cap) * 4;
         fkeys = (cpg + size_t(pg_cap) * 4 + 15) & ~size_t(15);
         const size_t ring = size_t(stages) * SelCfg<D>::STAGEB, fin = fkeys + (kFinKeys + 8) * 4;
-        tbl = ((ring > fin ? ring : fin) + 15) & ~size_t(15);
+        slk = ((ring > fin ? ring : fin) + 15) & ~size_t(15);
+        tbl = (slk + size_t(rows) * 4 + 15) & ~size_t(15);
         prm = tbl + SelCfg<D>::TBL;
         head = prm + SelCfg<D>::QB + SelCfg<D>::PB;
         total = (head + sizeof(SelHead) + 15) & ~size_t(15);
@@ -352,7 +429,8 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     constexpr int W = C::W, NG = D / 32;  // code words per row, 16-byte groups (32 channels) per row
     extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t stages = plan.stages, cand_cap = plan.cand_cap;
-    const SelLayout<D> lay(stages, cand_cap, plan.pg_cap);
+    const SelLayout<D> lay(stages, cand_cap, plan.pg_cap, plan.rows);
+    uint32_t* slk = reinterpret_cast<uint32_t*>(smem + lay.slk);
     unsigned char* ring = smem;
     float* tbl = reinterpret_cast<float*>(smem + lay.tbl);          // [D][16]
     unsigned char* prm_raw = smem + lay.prm;                         // q rows | scales | zps
@@ -376,6 +454,10 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     const uint32_t n_chunks = (ns + kSRows - 1) / kSRows;
     const bool trailing = !all;            // block N-1 is forced in (scored by the finalize)
     uint32_t* gkeys = sw.keys + du.seg;
+    // a unit whose keys need several finalize batches: each slice bounds its own
+    // ceil((K-1)/C)-th largest key, and the finalize takes T = min over the slices
+    // (one pass over the unit's keys instead of two histogram passes and a compaction)
+    const bool big = !all && K > 1 && Cn > 1 && nd > kFinKeys;
 
     SEL_TRACE(0);
     if (tid == 0) {
@@ -550,6 +632,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
                     if (ra < ns) {
                         const uint32_t k = uint32_t(I0) ^ 0x80000000u;
                         __stcg(gkeys + s0 + ra, k);
+                        if (big) slk[ra] = k;
                         kmin = min(kmin, k);
                         kmax = max(kmax, k);
                         if (diag_approx) diag_approx[du.seg + s0 + ra] = float(I0) * a_scale;
@@ -557,6 +640,7 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
                     if (rb < ns) {
                         const uint32_t k = uint32_t(I1) ^ 0x80000000u;
                         __stcg(gkeys + s0 + rb, k);
+                        if (big) slk[rb] = k;
                         kmin = min(kmin, k);
                         kmax = max(kmax, k);
                         if (diag_approx) diag_approx[du.seg + s0 + rb] = float(I1) * a_scale;
@@ -583,8 +667,26 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
                 kmin = min(kmin, __float_as_uint(sh.red[0][i]));
                 kmax = max(kmax, __float_as_uint(sh.red[1][i]));
             }
-            __stcg(sw.slot + 2 * blockIdx.x, kmin);
-            __stcg(sw.slot + 2 * blockIdx.x + 1, kmax);
+            __stcg(sw.slot + 4 * blockIdx.x, kmin);
+            __stcg(sw.slot + 4 * blockIdx.x + 1, kmax);
+            sh.st[10] = kmin;
+            sh.st[11] = kmax;
+        }
+        if (big) {  // this slice's bound t_r <= its kr-th largest key (0: none)
+            const uint32_t kr = (K - 1 + Cn - 1) / Cn;
+            uint32_t t_r = 0u;
+            cons_sync();
+            if (ns >= kr) {
+                const uint32_t smin = sh.st[10], span = sh.st[11] - smin;
+                const uint32_t shift = span < uint32_t(kBins) ? 0u : 32u - __clz(span) - 10u;
+#pragma unroll 4
+                for (uint32_t i = tid; i < ns; i += kSCons) atomicAdd(&sh.hist[(slk[i] - smin) >> shift], 1u);
+                cons_sync();
+                if (warp == 0) find_bin_desc(sh.hist, kr, lane, &sh.st[12], &sh.st[13]);
+                cons_sync();
+                t_r = smin + (sh.st[12] << shift);
+            }
+            if (tid == 0) __stcg(sw.slot + 4 * blockIdx.x + 2, t_r);
         }
         SEL_TRACE(6);
     }
@@ -635,16 +737,19 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
         for (uint32_t i = tid; i < G * D / 8; i += kSThreads)
             reinterpret_cast<uint4*>(q_copy + size_t(u) * G * D)[i] = reinterpret_cast<const uint4*>(qrows)[i];
     if (warp == kSWarps - 1) {  // the unit's key range: min / max over its slices
-        uint32_t mn = 0xffffffffu, mx = 0u;
+        uint32_t mn = 0xffffffffu, mx = 0u, bnd = 0xffffffffu;
         for (uint32_t i = lane; i < Cn; i += 32) {
-            mn = min(mn, __ldcg(sw.slot + 2 * (sd.first + i)));
-            mx = max(mx, __ldcg(sw.slot + 2 * (sd.first + i) + 1));
+            mn = min(mn, __ldcg(sw.slot + 4 * (sd.first + i)));
+            mx = max(mx, __ldcg(sw.slot + 4 * (sd.first + i) + 1));
+            bnd = min(bnd, __ldcg(sw.slot + 4 * (sd.first + i) + 2));
         }
         mn = __reduce_min_sync(0xffffffffu, mn);
         mx = __reduce_max_sync(0xffffffffu, mx);
+        bnd = __reduce_min_sync(0xffffffffu, bnd);
         if (lane == 0) {
             sh.st[7] = mn;
             sh.st[8] = mx;
+            sh.st[14] = bnd;
         }
     } else {  // exact product table: warp w < 8 builds 16 channels x 16 codes
         constexpr uint32_t CPT = 16 * D / 8 / 32;  // codes per lane
@@ -663,7 +768,10 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     const uint32_t e_int = sh.st[0];
     const bool one_batch = nd <= kFinKeys;
     uint32_t thr = 0u;
-    if (!all && K > 1) {
+    if (big) {
+        const uint32_t T = sh.st[14];  // min over the slices' bounds: >= K-1 keys are >= T
+        thr = (e_int == 0xffffffffu || T < 2ull * e_int) ? 0u : T - 2u * e_int;
+    } else if (!all && K > 1) {
         // T = lower edge of the histogram bin holding the (K-1)-th largest key, refined once
         // inside that bin: at least K-1 keys are >= T (a lower bound of the (K-1)-th largest;
         // exact when the second-level bins are one key value wide)
@@ -749,25 +857,51 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
     // prefetched into shared memory for the emit below
     const uint32_t n_sc = n <= cand_cap ? n + (trailing ? 1u : 0u) : (trailing ? 1u : 0u);
     const bool pg_pre = pages.page && n <= cand_cap && (n + 1) * ppb <= plan.pg_cap;
-    for (uint32_t j = tid; j < n_sc; j += kSThreads) {
-        const bool tr = n > cand_cap || j == n;  // the trailing block
-        const uint32_t i = tr ? N - 1 : list[j];
-        const uint32_t slot = tr ? n : j;
-        uint32_t wd[W];
-        load_row_global<W>(L.codes, du.seg + i, i, wd);
-        if (pg_pre || (tr && pages.page)) {
-#pragma unroll 1
-            for (uint32_t pp = 0; pp < ppb; ++pp) {
-                const uint32_t t0 = i * du.block + pp * L.P;
-                const uint32_t pg = t0 < du.n_tokens ? head_base + __ldg(pt + t0 / L.P) : 0u;
-                if (tr) sh.tpg[pp] = pg;
-                else cpg[slot * ppb + pp] = pg;
-            }
+    // Rows in batches of the dead key buffer (512 rows at d = 128): every candidate row of
+    // a batch is requested at once (16-byte cp.async pieces, as stored: swizzled), so a
+    // batch costs one L2 round trip whatever the candidates per thread
+    constexpr uint32_t kRowBatch = kFinKeys * 4 / C::ROWB;
+    unsigned char* rowbuf = reinterpret_cast<unsigned char*>(skeys);
+    for (uint32_t j0 = 0; j0 < n_sc; j0 += kRowBatch) {
+        const uint32_t jn = min(n_sc, j0 + kRowBatch);
+        __syncthreads();  // the key batch (or the previous row batch) is dead
+        for (uint32_t e = tid; e < (jn - j0) * (W / 4); e += kSThreads) {
+            const uint32_t jj = j0 + e / (W / 4), g = e % (W / 4);
+            const uint32_t i = (n > cand_cap || jj == n) ? N - 1 : list[jj];
+            cp_async16(smem_u32(rowbuf + (jj - j0) * C::ROWB + g * 16), L.codes + (du.seg + i) * W + g * 4);
         }
-        const float x = exact_row<W>(wd, tbl);
-        const unsigned long long comp = (uint64_t(order_key(x)) << 32) | uint32_t(~i);
-        if (tr) sh.ct = comp;
-        else cand[slot] = comp;
+        cp_async_commit();
+        cp_async_wait0();
+        __syncthreads();
+        for (uint32_t j = j0 + tid; j < jn; j += kSThreads) {
+            const bool tr = n > cand_cap || j == n;  // the trailing block
+            const uint32_t i = tr ? N - 1 : list[j];
+            const uint32_t slot = tr ? n : j;
+            if (pg_pre || (tr && pages.page)) {
+#pragma unroll 1
+                for (uint32_t pp = 0; pp < ppb; ++pp) {
+                    const uint32_t t0 = i * du.block + pp * L.P;
+                    const uint32_t pg = t0 < du.n_tokens ? head_base + __ldg(pt + t0 / L.P) : 0u;
+                    if (tr) sh.tpg[pp] = pg;
+                    else cpg[slot * ppb + pp] = pg;
+                }
+            }
+            uint32_t wd[W];
+            const unsigned char* src = rowbuf + (j - j0) * C::ROWB;
+            const uint32_t key = code_row_key(i, W);
+#pragma unroll
+            for (int g = 0; g < W / 4; ++g) {
+                const uint4 v = *reinterpret_cast<const uint4*>(src + ((g ^ key) << 4));
+                wd[4 * g] = v.x;
+                wd[4 * g + 1] = v.y;
+                wd[4 * g + 2] = v.z;
+                wd[4 * g + 3] = v.w;
+            }
+            const float x = exact_row<W>(wd, tbl);
+            const unsigned long long comp = (uint64_t(order_key(x)) << 32) | uint32_t(~i);
+            if (tr) sh.ct = comp;
+            else cand[slot] = comp;
+        }
     }
     __syncthreads();
     SEL_TRACE(9);
@@ -820,12 +954,31 @@ __global__ void __launch_bounds__(kSThreads, 2) k_select(LayerView L, const uint
             above = trailing && me > ct;
             emit(rank + (trailing && ct > me ? 1u : 0u), ~uint32_t(me), j);
         }
-    } else {  // large candidate sets (large budgets): sort, then emit by position
-        sort_desc(cand, n);  // positions change: pages are resolved from the page table
+    } else if (n <= 1024u && lay.fkeys >= 1024u * 8u) {  // large sets (large budgets): sort (the 1024
+        // padded composites may overwrite the dead candidate list / pages), emit by position
+        sort1024_desc(cand, n);
         for (uint32_t p = tid; p < K1; p += kSThreads) {
             const unsigned long long me = cand[p];
             if (trailing && me > ct) atomicAdd(&sh.nsel, 1u);
             emit(p + (trailing && ct > me ? 1u : 0u), ~uint32_t(me), kNoPrefetch);
+        }
+    } else {  // every thread ranks several candidates
+        for (uint32_t j = tid; j < n; j += kSThreads) {
+            const unsigned long long me = cand[j];
+            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+            uint32_t o = 0;
+            for (; o + 4 <= n; o += 4) {
+                r0 += cand[o] > me;
+                r1 += cand[o + 1] > me;
+                r2 += cand[o + 2] > me;
+                r3 += cand[o + 3] > me;
+            }
+            for (; o < n; ++o) r0 += cand[o] > me;
+            const uint32_t rank = (r0 + r1) + (r2 + r3);
+            if (rank < K1) {
+                if (trailing && me > ct) atomicAdd(&sh.nsel, 1u);
+                emit(rank + (trailing && ct > me ? 1u : 0u), ~uint32_t(me), j);
+            }
         }
     }
     SEL_TRACE(10);
@@ -857,8 +1010,9 @@ bool select_fused_supported(const LayerView& L) {
     return L.bits == 4 && L.method == ABSP_CENTROID_MEAN && (L.D == 64 || L.D == 128) && L.G <= 8;
 }
 
-size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_t pg_cap) {
-    return D == 64 ? SelLayout<64>(stages, cand_cap, pg_cap).total : SelLayout<128>(stages, cand_cap, pg_cap).total;
+size_t select_fused_smem(uint32_t D, uint32_t stages, uint32_t cand_cap, uint32_t pg_cap, uint32_t rows) {
+    return D == 64 ? SelLayout<64>(stages, cand_cap, pg_cap, rows).total
+                   : SelLayout<128>(stages, cand_cap, pg_cap, rows).total;
 }
 
 // Slices of a layout: the smallest slice size S (a multiple of 256 rows, at most 4096)
@@ -880,8 +1034,8 @@ SelectPlan plan_select(const std::vector<UnitDesc>& desc, uint32_t max_budget, u
     while (p.cand_cap < kCandCapMax && p.cand_cap < 4 * max_budget) p.cand_cap <<= 1;
     p.pg_cap = 4096;
     for (p.stages = kSStages; p.stages > 2; --p.stages)
-        if (select_fused_smem(D, p.stages, p.cand_cap, p.pg_cap) * 2 + 2048 <= 228 * 1024) break;
-    p.ok = select_fused_smem(D, p.stages, p.cand_cap, p.pg_cap) <= 227 * 1024;
+        if (select_fused_smem(D, p.stages, p.cand_cap, p.pg_cap, p.rows) * 2 + 2048 <= 228 * 1024) break;
+    p.ok = select_fused_smem(D, p.stages, p.cand_cap, p.pg_cap, p.rows) <= 227 * 1024;
     if (slices) {
         slices->clear();
         for (uint32_t u = 0; u < desc.size(); ++u) {
@@ -911,7 +1065,7 @@ cudaError_t launch_select_fused(const LayerView& L, const uint16_t* q, const Sel
                                 uint32_t* blocks, uint32_t stride, uint32_t* counts, const PageList& pages,
                                 uint32_t* ready, float* diag_approx, float* diag_err, uint16_t* q_copy, cudaStream_t s,
                                 int* launches) {
-    const size_t smem = select_fused_smem(L.D, plan.stages, plan.cand_cap, plan.pg_cap);
+    const size_t smem = select_fused_smem(L.D, plan.stages, plan.cand_cap, plan.pg_cap, plan.rows);
     cudaError_t e;
     if (L.D == 64)
         e = launch_pdl(k_select<64>, dim3(plan.n_slices), dim3(kSThreads), smem, s, L, q, plan, work, blocks, stride,
