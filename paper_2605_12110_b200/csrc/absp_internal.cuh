@@ -173,8 +173,9 @@ cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList&
                           int* launches);
 size_t attend_smem_bytes(uint32_t D, uint32_t P);
 // Fused decode-step selection (select.cu): estimate + select + page resolution per
-// (sequence, KV head) unit in one kernel, one cluster of `cluster` CTAs per unit; the
-// same ordered selections as launch_score + launch_topk (INT4 mean stores).
+// (sequence, KV head) unit in one kernel over balanced slices of the units' centroids
+// (the last slice of a unit to finish finalizes it); the same ordered selections as
+// launch_score + launch_topk (INT4 mean stores).
 bool select_fused_supported(const LayerView& L);
 // One slice of the fused selection: rows [r nd / n, (r + 1) nd / n) of unit `unit`'s
 // candidate domain (nd = N, or N - 1 when the trailing block is forced), one CTA each;
@@ -219,6 +220,10 @@ cudaError_t launch_recall(const LayerView& L, uint32_t max_nblocks, const double
                           cudaStream_t s, int* launches);
 cudaError_t launch_fill_synth(uint16_t* dst, uint64_t count, uint64_t seed, uint64_t stream_id,
                               cudaStream_t s);
+
+// Per-unit ready flags sit one per 128-byte line (flag u at ready[u * kReadyStride]): the
+// attention producers poll them while the selection publishes, spread over L2 slices.
+constexpr uint32_t kReadyStride = 32;
 
 // Rows per attention chunk (one pipeline stage), see attend.cu.
 constexpr uint32_t kAttnChunkRows = 128;

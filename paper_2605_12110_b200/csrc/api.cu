@@ -552,10 +552,10 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
     l->sel_stride = ceil_div(c.token_budget, c.candidate_block_sizes[0]);
     ABSP_CUDA(l->sel_blocks.ensure(units * l->sel_stride));
     ABSP_CUDA(l->sel_counts.ensure(units));
-    ABSP_CUDA(l->ready.ensure(units));
+    ABSP_CUDA(l->ready.ensure(units * kReadyStride));
     ABSP_CUDA(l->scored.ensure(units));
     if (!async) {  // zero between steps; the step kernels keep them so
-        ABSP_CUDA(cudaMemset(l->ready.p, 0, units * 4));
+        ABSP_CUDA(cudaMemset(l->ready.p, 0, units * kReadyStride * 4));
         ABSP_CUDA(cudaMemset(l->scored.p, 0, units * 4));
     }
     Stager& up = l->stager;

@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             }
             if (ready && f.u != pu) {  // decode step: the unit's page list must be published
                 pu = f.u;
-                while (ld_acquire(ready + pu) == 0u) __nanosleep(32);
+                for (uint32_t ns = 32; ld_acquire(ready + size_t(pu) * kReadyStride) == 0u; ns = min(2 * ns, 256u))
+                    __nanosleep(ns);
                 // the unit's q rows may have been written by the selection with generic
                 // stores (host-resident q, select.cu q_copy): order them before our TMA reads
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
                                                           acc[3 % PER] * inv);
         else
             *reinterpret_cast<float2*>(dst) = make_float2(acc[0] * inv, acc[1 % PER] * inv);
-        if (ready && h == 0 && lane == 0) ready[mu] = 0u;  // every producer is past mu: re-arm
+        if (ready && h == 0 && lane == 0) ready[size_t(mu) * kReadyStride] = 0u;  // every producer is past mu: re-arm
     };
 
     // End of a run: the 8 warps combine their states into the run's single partial

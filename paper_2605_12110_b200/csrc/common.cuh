@@ -88,7 +88,7 @@ __device__ __forceinline__ void publish_selection(const LayerView& L, const Unit
     if (!ready) return;
     __syncthreads();
     if (threadIdx.x == 0)
-        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(ready + u), "r"(1u) : "memory");
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(ready + size_t(u) * kReadyStride), "r"(1u) : "memory");
 }
 
 }  // namespace absp
