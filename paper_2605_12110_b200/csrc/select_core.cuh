@@ -14,7 +14,7 @@
 
 namespace absp {
 namespace selcore {
-namespace {  // internal linkage: the header is compiled into select.cu and attend.cu
+namespace {  // internal linkage (device helpers defined in a header)
 
 constexpr int kSCons = 256;              // consumer threads (8 warps), one code row each per stage
 constexpr int kSThreads = kSCons + 32;   // + producer warp
