@@ -14,6 +14,8 @@
 #include <map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "absp_internal.cuh"
 
 using namespace absp;
@@ -21,6 +23,13 @@ using namespace absp;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over one C-ABI call (visible under Nsight Systems / ncu --nvtx; a few
+// nanoseconds when no tool is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 absp_status fail(absp_status st, const std::string& msg) {
     g_err = msg;
@@ -785,6 +794,7 @@ absp_status absp_kv_bind(absp_ctx* ctx, uint32_t layer, const void* k_pool, cons
 }
 
 absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream) {
+    NvtxRange nvtx_("absp_build_store");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -799,6 +809,7 @@ absp_status absp_build_store(absp_ctx* ctx, uint32_t layer, void* stream) {
 }
 
 absp_status absp_append(absp_ctx* ctx, uint32_t layer, const void* k_new, const void* v_new, void* stream) {
+    NvtxRange nvtx_("absp_append");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -868,6 +879,7 @@ static absp_status do_attend_step(absp_ctx* ctx, Layer* l, const void* q, float*
 
 absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* blocks,
                         uint32_t blocks_stride, uint32_t* counts, void* stream) {
+    NvtxRange nvtx_("absp_select");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -884,6 +896,7 @@ absp_status absp_select(absp_ctx* ctx, uint32_t layer, const void* q, uint32_t* 
 
 absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint32_t* blocks,
                         uint32_t blocks_stride, const uint32_t* counts, float* out, void* stream) {
+    NvtxRange nvtx_("absp_attend");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -918,6 +931,7 @@ absp_status absp_attend(absp_ctx* ctx, uint32_t layer, const void* q, const uint
 
 absp_status absp_attend_selected(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
                                  void* stream) {
+    NvtxRange nvtx_("absp_attend_selected");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -948,6 +962,7 @@ absp_status absp_attend_validate(absp_ctx* ctx, uint32_t layer, void* stream) {
 
 absp_status absp_full_attention(absp_ctx* ctx, uint32_t layer, const void* q, float* out, double* weights,
                                 uint64_t weights_stride, void* stream) {
+    NvtxRange nvtx_("absp_full_attention");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -982,6 +997,7 @@ absp_status absp_full_attention(absp_ctx* ctx, uint32_t layer, const void* q, fl
 absp_status absp_attention_recall(absp_ctx* ctx, uint32_t layer, const double* weights, uint64_t weights_stride,
                                   const uint32_t* blocks, uint32_t blocks_stride, const uint32_t* counts,
                                   double* recall, void* stream) {
+    NvtxRange nvtx_("absp_attention_recall");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -1035,6 +1051,7 @@ static absp_status step_select(absp_ctx* ctx, Layer* l, const void* q, uint32_t*
 }
 
 absp_status absp_select_step(absp_ctx* ctx, uint32_t layer, const void* q, void* stream) {
+    NvtxRange nvtx_("absp_select_step");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -1046,6 +1063,7 @@ absp_status absp_select_step(absp_ctx* ctx, uint32_t layer, const void* q, void*
 
 absp_status absp_decode_step(absp_ctx* ctx, uint32_t layer, const void* q, float* out,
                              void* stream) {
+    NvtxRange nvtx_("absp_decode_step");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;
@@ -1137,6 +1155,7 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
 
 absp_status absp_decode_step_host(absp_ctx* ctx, uint32_t layer, const void* q_host,
                                   float* out_host, void* stream) {
+    NvtxRange nvtx_("absp_decode_step_host");
     Layer* l;
     absp_status st = get_layer(ctx, layer, &l);
     if (st != ABSP_OK) return st;

@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "absp_internal.cuh"
 
 namespace absp {
@@ -103,6 +105,8 @@ using namespace absp;
 extern "C" absp_status absp_profile_sample(int device, const absp_config* config, const float* keys,
                                            const float* values, const float* queries, uint64_t seq_len,
                                            const uint32_t* assignment, double* recalls, double* assigned_recall) {
+    nvtxRangePushA("absp_profile_sample");
+    struct Pop { ~Pop() { nvtxRangePop(); } } nvtx_pop_;
     if (!config || !keys || !values || !queries || !recalls)
         return cfail(ABSP_EINVAL, "profile_sample: null pointer");
     CAL_ABI(absp_config_validate(config));

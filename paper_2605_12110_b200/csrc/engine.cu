@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "absp_internal.cuh"
 
 namespace absp {
@@ -194,6 +196,8 @@ absp_status absp_engine_destroy(absp_engine* e) {
 
 absp_status absp_engine_prefill(absp_engine* e, const float* keys, uint64_t keys_len, const float* values,
                                 uint64_t values_len, uint64_t num_tokens) {
+    nvtxRangePushA("absp_engine_prefill");
+    struct Pop { ~Pop() { nvtxRangePop(); } } nvtx_pop_;
     if (!e) return efail(ABSP_EINVAL, "null engine");
     if (e->prefilled) return efail(ABSP_ESTATE, "prefill: engine already prefilled");  // engine.cpp:416
     const uint64_t H = e->cfg.num_kv_heads, D = e->cfg.head_dim, P = e->cfg.page_size;
@@ -236,6 +240,8 @@ absp_status absp_engine_prefill(absp_engine* e, const float* keys, uint64_t keys
 absp_status absp_engine_step(absp_engine* e, const float* keys, uint64_t keys_len, const float* values,
                              uint64_t values_len, const float* query, uint64_t query_len, float* out,
                              uint32_t* blocks, uint32_t blocks_stride, uint32_t* counts, int* full_attention_fallback) {
+    nvtxRangePushA("absp_engine_step");
+    struct Pop { ~Pop() { nvtxRangePop(); } } nvtx_pop_;
     if (!e) return efail(ABSP_EINVAL, "null engine");
     if (!e->prefilled) return efail(ABSP_ESTATE, "step: call prefill first");  // engine.cpp:444
     const uint64_t H = e->cfg.num_kv_heads, D = e->cfg.head_dim, Hq = e->cfg.num_q_heads;
