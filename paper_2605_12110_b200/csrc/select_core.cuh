@@ -491,7 +491,7 @@ __device__ __forceinline__ void finalize_unit(const FinIn<D>& a, SelHead& sh) {
         for (uint32_t i = lane; i < a.Cn; i += 32) {
             mn = min(mn, __ldcg(a.sw.slot + 4 * (a.first + i)));
             mx = max(mx, __ldcg(a.sw.slot + 4 * (a.first + i) + 1));
-            bnd = min(bnd, __ldcg(a.sw.slot + 4 * (a.first + i) + 2));
+            if (big) bnd = min(bnd, __ldcg(a.sw.slot + 4 * (a.first + i) + 2));  // written by big units' slices
         }
         mn = __reduce_min_sync(0xffffffffu, mn);
         mx = __reduce_max_sync(0xffffffffu, mx);
