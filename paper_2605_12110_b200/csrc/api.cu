@@ -665,9 +665,10 @@ absp_status absp_config_validate(const absp_config* cfg) {
         return fail(ABSP_EINVAL, "this build supports head_dim 64 or 128");
     if (maxc > kAttnChunkRows)
         return fail(ABSP_EINVAL, "block sizes above 128 are not supported by this build");
-    for (uint32_t i = 0; i < c.num_candidates; ++i)
-        if (c.candidate_block_sizes[i] & (c.candidate_block_sizes[i] - 1))
-            return fail(ABSP_EINVAL, "this build supports power-of-two block sizes only");
+    // block sizes: any multiple of page_size up to 128 (the reference's rule, checked
+    // above); pages: a power of two dividing the 128-row attention chunk
+    if ((c.page_size & (c.page_size - 1)) || c.page_size > kAttnChunkRows)
+        return fail(ABSP_EINVAL, "this build supports power-of-two page sizes up to 128 only");
     if (c.max_batch == 0 || c.max_seq_len == 0 || c.num_layers == 0)
         return fail(ABSP_EINVAL, "max_batch, max_seq_len and num_layers must be positive");
     const uint32_t minc = c.candidate_block_sizes[0];

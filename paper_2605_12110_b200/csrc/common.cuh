@@ -38,34 +38,44 @@ struct CodeOffsets {
     }
 };
 
+// Page-list slot of page pp of selection entry e: a 128-row attention chunk holds
+// E = floor(128 / B) whole blocks of ppb = B / P pages in its NS = 128 / P slots, so
+// entry e sits in chunk e / E at slot (e % E) * ppb + pp (the chunk's last
+// NS - E * ppb slots stay empty when B does not divide 128). When B divides 128 this
+// is e * ppb + pp.
+__host__ __device__ __forceinline__ uint32_t page_slot(uint32_t e, uint32_t pp, uint32_t E, uint32_t ppb,
+                                                       uint32_t ns) {
+    return (e / E) * ns + (e % E) * ppb + pp;
+}
+
 // Resolve the ordered selection `out` (global or shared) of unit u to pool pages
 // for the attention producer (the reference's populate_page_spans,
-// engine.cpp:271-283): slot s = entry * (B/P) + page; slots up to the end of the
-// unit's last 128-row attention chunk are written, empty ones with valid = 0.
-// Block sizes and P are powers of two (checked by absp_config_validate). Starts
-// with a CTA barrier so `out` written by this CTA is visible.
+// engine.cpp:271-283): every slot of the unit's chunks is written (page_slot), empty
+// ones with valid = 0. Starts with a CTA barrier so `out` written by this CTA is
+// visible.
 __device__ __forceinline__ void resolve_pages(const LayerView& L, const UnitDesc& du, uint32_t u,
                                               uint32_t sel_total, const uint32_t* out,
                                               const PageList& pages) {
     if (!pages.page) return;
-    const uint32_t ppb_log = __ffs(du.block) - __ffs(L.P);  // log2(B / P)
-    const uint32_t p_log = __ffs(L.P) - 1;
+    const uint32_t ppb = du.block / L.P;
     const uint32_t E = kAttnChunkRows / du.block;
-    const uint32_t slot_end = ((sel_total + E - 1) / E * E) << ppb_log;
+    const uint32_t ns = pages.ns;
+    const uint32_t slot_end = ((sel_total + E - 1) / E) * ns;
     const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
     const uint32_t head_base = du.head * uint32_t(L.pool_pages);
-    const size_t base = size_t(pages.chunk_base[u]) * pages.ns;
+    const size_t base = size_t(pages.chunk_base[u]) * ns;
     uint32_t* pg = pages.page + base;
     uint16_t* vl = pages.valid + base;
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
-        const uint32_t e = s >> ppb_log, pp = s & ((1u << ppb_log) - 1u);
+        const uint32_t w = s % ns, ein = w / ppb, pp = w % ppb;
+        const uint32_t e = (s / ns) * E + ein;
         uint32_t v = 0, page = 0;
-        if (e < sel_total) {
-            const uint32_t t0 = out[e] * du.block + (pp << p_log);
+        if (ein < E && e < sel_total) {
+            const uint32_t t0 = out[e] * du.block + pp * L.P;
             if (t0 < du.n_tokens) {
                 v = min(L.P, du.n_tokens - t0);
-                page = head_base + __ldg(pt + (t0 >> p_log));
+                page = head_base + __ldg(pt + t0 / L.P);
             }
         }
         pg[s] = page;

@@ -669,6 +669,7 @@ __device__ __forceinline__ void finalize_unit(const FinIn<D>& a, SelHead& sh) {
     // straight into the attention producer's page list.
     const uint32_t n_sel = trailing ? K : n;
     const size_t pbase = pages.page ? size_t(pages.chunk_base[u]) * pages.ns : 0;
+    const uint32_t E = kAttnChunkRows / du.block;  // entries per attention chunk (page_slot)
     // j: candidate index (pages in cpg), kNoPrefetch (page table), ~0u: the trailing block
     auto emit = [&](uint32_t p, uint32_t blk, uint32_t j) {
         blocks[size_t(u) * stride + p] = blk;
@@ -682,8 +683,9 @@ __device__ __forceinline__ void finalize_unit(const FinIn<D>& a, SelHead& sh) {
                 page = j == ~0u ? sh.tpg[pp] : (pg_pre && j != kNoPrefetch) ? cpg[j * ppb + pp]
                                                                             : head_base + __ldg(pt + t0 / L.P);
             }
-            pages.page[pbase + size_t(p) * ppb + pp] = page;
-            pages.valid[pbase + size_t(p) * ppb + pp] = uint16_t(v);
+            const uint32_t slot = page_slot(p, pp, E, ppb, pages.ns);
+            pages.page[pbase + slot] = page;
+            pages.valid[pbase + slot] = uint16_t(v);
         }
     };
     bool above = false;  // a winner ranked before the trailing block
@@ -735,12 +737,12 @@ __device__ __forceinline__ void finalize_unit(const FinIn<D>& a, SelHead& sh) {
     uint32_t n_above = __syncthreads_count(above);
     if (n > uint32_t(kSThreads)) n_above = sh.nsel;  // (set before the barrier above)
     if (trailing && tid == 0) emit(n_above, N - 1, ~0u);
-    if (pages.page) {  // the rest of the unit's last attention chunk: empty slots
-        const uint32_t E = kAttnChunkRows / du.block;
-        const uint32_t slot_end = ((n_sel + E - 1) / E * E) * ppb;
-        for (uint32_t s = n_sel * ppb + tid; s < slot_end; s += kSThreads) {
-            pages.page[pbase + s] = 0u;
-            pages.valid[pbase + s] = 0u;
+    if (pages.page) {  // the entries left in the unit's last attention chunk: empty slots
+        const uint32_t e_end = (n_sel + E - 1) / E * E;
+        for (uint32_t s = tid; s < (e_end - n_sel) * ppb; s += kSThreads) {
+            const uint32_t slot = page_slot(n_sel + s / ppb, s % ppb, E, ppb, pages.ns);
+            pages.page[pbase + slot] = 0u;
+            pages.valid[pbase + slot] = 0u;
         }
     }
     if (tid == 0) counts[u] = n_sel;

@@ -746,14 +746,15 @@ __global__ void k_resolve_pages(LayerView L, const uint32_t* __restrict__ blocks
         if (raw == 0) flags |= kAttendErrEmpty;
         if (raw > stride) flags |= kAttendErrCount;
     }
-    const uint32_t slot_end = ((cap + E - 1) / E) * E * ppb;
+    const uint32_t slot_end = ((cap + E - 1) / E) * pages.ns;  // every slot of the unit's chunks (page_slot)
     const uint32_t* pt = L.page_table + size_t(du.seq) * L.max_pages;
     const uint32_t head_base = du.head * uint32_t(L.pool_pages);
     const size_t base = size_t(pages.chunk_base[u]) * pages.ns;
     for (uint32_t s = threadIdx.x; s < slot_end; s += blockDim.x) {
-        const uint32_t e = s / ppb, pp = s % ppb;
+        const uint32_t w = s % pages.ns, ein = w / ppb, pp = w % ppb;
+        const uint32_t e = (s / pages.ns) * E + ein;
         uint32_t v = 0, page = 0;
-        if (e < cnt) {
+        if (ein < E && e < cnt) {
             const uint32_t blk = __ldg(blocks + size_t(u) * stride + e);
             if (blk >= du.n_blocks) {
                 flags |= kAttendErrBlock;

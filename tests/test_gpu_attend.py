@@ -67,6 +67,7 @@ def _attend(gl, selection, stride):
     (128, 8, 16, (16, 64), (6000, 100, 4097), 1),
     (64, 2, 16, (16, 32), (3000, 20), 5),                     # d = 64
     (128, 1, 4, (4, 16), (2500,), 200),                       # MHA, stride far above counts
+    (128, 4, 16, (16, 48, 112), (5000, 700), 3),              # blocks that do not divide the 128-row chunk
 ])
 def test_attend_random_selections_vs_oracle(cuda, d, G, P, cands, seq_lens, extra):
     from gpu_util import GpuLayer, within_tol

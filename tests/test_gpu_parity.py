@@ -82,6 +82,9 @@ def test_golden_cases(cuda, golden, name):
     (2, 4, 16, (16, 32, 64), (100, 2000), 4096),              # T >= n: every block selected
     (1, 2, 16, (16, 64), (3000, 700), 64),                    # K = 1 (B = 64 = T): the trailing block only
     (4, 8, 16, (16, 32, 64), (20000,) * 20, 2048),            # 160 units: one CTA per unit, slices recycled
+    (4, 8, 8, (8, 24, 40), (5000, 1234), 1024),               # block sizes that do not divide the 128-row
+    (4, 8, 16, (16, 48, 80, 112), (9000, 777), 2048),         #   attention chunk (any multiple of P, as the
+    (8, 4, 4, (12, 20), (3000,), 512),                        #   reference allows): chunks with empty slots
 ])
 def test_random_batches_vs_oracle(cuda, G, H, P, cands, seq_lens, T):
     from gpu_util import GpuLayer, within_tol
