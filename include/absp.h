@@ -125,7 +125,10 @@ typedef struct absp_layer_info {
 int absp_abi_version(void);
 const char* absp_last_error(void);
 
-/* EngineConfig::validate (config.cpp:48-78) plus the GPU build's own limits. */
+/* EngineConfig::validate (config.cpp:48-78) plus the GPU build's own limits:
+ * head_dim 64 or 128; GQA group size G <= 8; page_size a power of two <= 128; block
+ * sizes any multiple of page_size up to 128 (the reference's rule, capped at the
+ * 128-row attention chunk); token_budget / min block size <= 2048. */
 absp_status absp_config_validate(const absp_config* cfg);
 
 absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out);
