@@ -509,15 +509,13 @@ static absp_status layout_layer(absp_ctx* ctx, Layer* l, cudaStream_t stream = n
             }
             return ctas;
         };
-        double lo = double(l->total_centroids) / grid, hi = double(l->total_centroids) / grid + 4 * kItemCost + 2;
-        while (cut(hi, false) > grid) hi *= 1.5;
-        for (int it = 0; it < 40; ++it) {  // smallest cap that fits the grid
-            const double mid = 0.5 * (lo + hi);
-            if (cut(mid, false) <= grid) hi = mid;
-            else lo = mid;
-        }
+        // per-CTA cost cap: the mean cost with one item per unit and one split per CTA
+        // boundary, raised by 1 % until the cut fits the grid (typically 1-3 passes; this
+        // runs on every append, so no bisection)
+        double cap = (double(l->total_centroids) + kItemCost * double(l->desc.size() + grid)) / grid;
+        while (cut(cap, false) > grid) cap *= 1.01;
         l->item_begin.assign(grid + 1, 0);
-        const uint64_t used = cut(hi, true);
+        const uint64_t used = cut(cap, true);
         for (uint64_t c = used; c < grid; ++c) l->item_begin[c] = uint32_t(l->items.size());  // idle CTAs
         l->item_begin[grid] = uint32_t(l->items.size());
     }

@@ -33,13 +33,15 @@ vn = torch.empty_like(kn)
 for t, s in ((q, 2), (kn, 3), (vn, 4)):
     fill_synthetic_bf16(t, SEED, s)
 out = torch.empty(B, H * G, d, dtype=torch.float32, device="cuda")
-times, steps = [], []
+times, steps, enq = [], [], []
 for i in range(extra - 1):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     da.append(0, kn[i], vn[i])
+    te = time.perf_counter()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
+    enq.append(te - t0)
     da.decode_step(0, q, out)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
@@ -47,5 +49,7 @@ for i in range(extra - 1):
     steps.append(t2 - t1)
 times.sort()
 steps.sort()
+enq.sort()
 print(f"append+refresh (batch {B}, {n}+ ctx): median {times[len(times) // 2] * 1e6:.1f} us, "
-      f"min {times[0] * 1e6:.1f} us; eager decode_step median {steps[len(steps) // 2] * 1e6:.1f} us")
+      f"min {times[0] * 1e6:.1f} us (host enqueue median {enq[len(enq) // 2] * 1e6:.1f} us); "
+      f"eager decode_step median {steps[len(steps) // 2] * 1e6:.1f} us")
