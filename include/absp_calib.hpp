@@ -12,6 +12,7 @@
  *     make_report
  *   absp::transfer_check                         <- calibrator.cpp:159-224 (per sample on the GPU)
  *   absp::topk_page_recall(_per_head)            <- calibrator.cpp:226-249
+ *   absp::write_recall_csv, write_min_block_csv  <- calibrator.cpp:253-275
  *
  * The loops over samples and the Eq.-2 assignment rule are host code, as in the
  * reference; each sample's dense fp64 oracle, stores, selections and recall sums run
@@ -22,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <iostream>
@@ -303,6 +305,27 @@ inline double topk_page_recall(const std::vector<std::vector<std::size_t>>& sele
     double acc = 0.0;
     for (double r : per) acc += r;
     return acc / double(per.size());
+}
+
+// CSV reports (calibrator.cpp:253-275): numbers as printf("%.10g").
+inline void write_recall_csv(const std::string& path, const RecallTable& table, const std::string& layer_tag) {
+    std::ofstream out(path, std::ios::trunc);
+    if (!out) throw std::runtime_error("write_recall_csv: cannot open " + path);
+    out << "head,layer,block_size,recall\n";
+    char buf[64];
+    for (std::size_t h = 0; h < table.num_heads; ++h)
+        for (std::size_t ci = 0; ci < table.candidates.size(); ++ci) {
+            std::snprintf(buf, sizeof(buf), "%.10g", table.at(h, ci));
+            out << h << ',' << layer_tag << ',' << table.candidates[ci] << ',' << buf << '\n';
+        }
+}
+
+inline void write_min_block_csv(const std::string& path, const std::vector<std::size_t>& min_block_sizes,
+                                const std::string& layer_tag) {
+    std::ofstream out(path, std::ios::trunc);
+    if (!out) throw std::runtime_error("write_min_block_csv: cannot open " + path);
+    out << "head,layer,min_block_size\n";
+    for (std::size_t h = 0; h < min_block_sizes.size(); ++h) out << h << ',' << layer_tag << ',' << min_block_sizes[h] << '\n';
 }
 
 }  // namespace absp

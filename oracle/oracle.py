@@ -104,6 +104,8 @@ def ref() -> C.CDLL:
                                               _sz, _sz, _f32p, _f32p, _f32p, _f64p]
         L.ref_transfer_check.argtypes = [_sz, _sz, _sz, C.POINTER(_sz), _sz, _sz, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(_sz), _sz, _sz, _f32p, _f32p, _f32p, _f64p]
+        L.ref_write_recall_csv.argtypes = [C.c_char_p, _sz, C.POINTER(_sz), _sz, _f64p, C.c_char_p]
+        L.ref_write_min_block_csv.argtypes = [C.c_char_p, C.POINTER(_sz), _sz, C.c_char_p]
         L.ref_assign_block_sizes.argtypes = [_sz, C.POINTER(_sz), _sz, _f64p, C.c_double, C.POINTER(_sz)]
         L.ref_config_validate.argtypes = [_sz, _sz, _sz, C.POINTER(_sz), _sz, _sz, C.c_int]
         L.ref_generate_synthetic.argtypes = [_sz, _sz, _sz, C.POINTER(C.c_int), C.POINTER(_sz),
@@ -483,3 +485,13 @@ def ref_assign_block_sizes(recalls, cands, tau):
     out = (_sz * H)()
     _rcheck(ref().ref_assign_block_sizes(H, (_sz * len(cands))(*cands), len(cands), recalls, tau, out))
     return [int(x) for x in out]
+
+
+def ref_write_recall_csv(path, recalls, cands, tag):
+    recalls = np.ascontiguousarray(recalls, np.float64)
+    _rcheck(ref().ref_write_recall_csv(str(path).encode(), recalls.shape[0], (_sz * len(cands))(*cands), len(cands),
+                                       recalls, tag.encode()))
+
+
+def ref_write_min_block_csv(path, sizes, tag):
+    _rcheck(ref().ref_write_min_block_csv(str(path).encode(), (_sz * len(sizes))(*sizes), len(sizes), tag.encode()))

@@ -469,6 +469,21 @@ int ref_transfer_check(size_t H, size_t d, size_t P, const size_t* cands, size_t
     });
 }
 
+int ref_write_recall_csv(const char* path, size_t H, const size_t* cands, size_t nc, const double* recalls,
+                         const char* tag) {
+    return guard([&] {
+        RecallTable t;
+        t.num_heads = H;
+        t.candidates.assign(cands, cands + nc);
+        t.recalls.assign(recalls, recalls + H * nc);
+        write_recall_csv(path, t, tag);
+    });
+}
+
+int ref_write_min_block_csv(const char* path, const size_t* sizes, size_t H, const char* tag) {
+    return guard([&] { write_min_block_csv(path, std::vector<std::size_t>(sizes, sizes + H), tag); });
+}
+
 int ref_assign_block_sizes(size_t H, const size_t* cands, size_t nc, const double* recalls, double tau,
                            size_t* out) {
     return guard([&] {

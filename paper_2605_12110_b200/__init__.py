@@ -7,7 +7,8 @@ from .absparse import (BlockAssignment, CentroidMethod, DecodeAttention, DecodeE
                        QuantMode, QuantSpec, StepResult, build_offsets, fill_synthetic_bf16)
 from .calibration import (CalibrationReport, RecallTable, Trace, TransferReport, assign_block_sizes,  # noqa: F401
                           load_trace, make_report, normalized_recall, profile_sample, profile_sensitivity,
-                          save_trace, topk_page_recall, topk_page_recall_per_head, transfer_check)
+                          save_trace, topk_page_recall, topk_page_recall_per_head, transfer_check,
+                          write_min_block_csv, write_recall_csv)
 from ._abi import (AbspError, CapacityError, CudaError, InvalidArgument, LogicError,  # noqa: F401
                    OutOfRange)
 
@@ -16,4 +17,4 @@ __all__ = ["BlockAssignment", "CentroidMethod", "DecodeAttention", "DecodeEngine
            "CudaError", "InvalidArgument", "LogicError", "OutOfRange", "CalibrationReport", "RecallTable", "Trace",
            "TransferReport", "assign_block_sizes", "load_trace", "make_report", "normalized_recall",
            "profile_sample", "profile_sensitivity", "save_trace", "topk_page_recall", "topk_page_recall_per_head",
-           "transfer_check"]
+           "transfer_check", "write_min_block_csv", "write_recall_csv"]

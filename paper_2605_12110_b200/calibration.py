@@ -10,6 +10,7 @@ Reference (/root/reference/proj):
   normalized_recall, make_report            calibrator.cpp:142-157
   transfer_check                            calibrator.cpp:159-224 -> GPU per sample
   topk_page_recall(_per_head)               calibrator.cpp:226-249
+  write_recall_csv, write_min_block_csv     calibrator.cpp:253-275
 
 The heavy work of a sample (the dense fp64 oracle with weights, a store + selection
 per candidate block size, the recall sums) runs in libabsp.so on the GPU; the loops
@@ -292,3 +293,33 @@ def topk_page_recall_per_head(selected: Sequence[Sequence[int]], reference: Sequ
 def topk_page_recall(selected, reference) -> float:
     per = topk_page_recall_per_head(selected, reference)
     return float(sum(per) / len(per)) if per else 0.0
+
+
+def _fmt10g(v: float) -> str:
+    """printf("%.10g") as the reference's format_double (calibrator.cpp:39-43)."""
+    return "%.10g" % v
+
+
+def write_recall_csv(path, table: RecallTable, layer_tag: str) -> None:
+    """CSV head,layer,block_size,recall (calibrator.cpp:253-264)."""
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise RuntimeError(f"write_recall_csv: cannot open {path}") from None
+    with f:
+        f.write("head,layer,block_size,recall\n")
+        for h in range(table.num_heads):
+            for ci, b in enumerate(table.candidates):
+                f.write(f"{h},{layer_tag},{b},{_fmt10g(table.at(h, ci))}\n")
+
+
+def write_min_block_csv(path, min_block_sizes: Sequence[int], layer_tag: str) -> None:
+    """CSV head,layer,min_block_size (calibrator.cpp:266-275)."""
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise RuntimeError(f"write_min_block_csv: cannot open {path}") from None
+    with f:
+        f.write("head,layer,min_block_size\n")
+        for h, b in enumerate(min_block_sizes):
+            f.write(f"{h},{layer_tag},{b}\n")

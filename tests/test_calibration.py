@@ -5,10 +5,11 @@ top-k page recall."""
 import numpy as np
 import pytest
 
-from oracle.oracle import RefError, ref_assign_block_sizes, ref_available, ref_load_trace, ref_save_trace
+from oracle.oracle import (RefError, ref_assign_block_sizes, ref_available, ref_load_trace, ref_save_trace,
+                           ref_write_min_block_csv, ref_write_recall_csv)
 from paper_2605_12110_b200 import (InvalidArgument, RecallTable, Trace, assign_block_sizes, load_trace,
                                    make_report, normalized_recall, save_trace, topk_page_recall,
-                                   topk_page_recall_per_head)
+                                   topk_page_recall_per_head, write_min_block_csv, write_recall_csv)
 
 needs_ref = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
 
@@ -86,3 +87,19 @@ def test_calibration_host_errors():
     assert topk_page_recall([[1, 2, 3], [5]], [[1, 2], [4]]) == 0.5
     with pytest.raises(InvalidArgument):
         topk_page_recall([[1]], [[]])
+
+
+@needs_ref
+def test_csv_reports_identical_to_reference(tmp_path):
+    rng = np.random.default_rng(9)
+    cands = [8, 16, 32, 64]
+    rec = rng.uniform(0.0, 1.0, (5, 4))
+    rec[0, 0], rec[1, 1], rec[2, 2] = 1.0, 1.0 / 3.0, 1e-12
+    table = RecallTable(5, cands, rec, 3)
+    write_recall_csv(tmp_path / "ours.csv", table, "0")
+    ref_write_recall_csv(tmp_path / "ref.csv", rec, cands, "0")
+    assert (tmp_path / "ours.csv").read_bytes() == (tmp_path / "ref.csv").read_bytes()
+    sizes = [8, 64, 16, 32, 8]
+    write_min_block_csv(tmp_path / "ours_m.csv", sizes, "layer3")
+    ref_write_min_block_csv(tmp_path / "ref_m.csv", sizes, "layer3")
+    assert (tmp_path / "ours_m.csv").read_bytes() == (tmp_path / "ref_m.csv").read_bytes()
