@@ -391,31 +391,32 @@ def run_absp(args, w, rank, world, local):
     step_bytes *= lps  # every layer of a step reads its own store and KV
     attn_bytes = attn_kv_bytes + B * Hl * G * d * (2 + 4)
 
-    # one CUDA graph per step (select + attend of lps layers) and, per layer,
-    # attention-only and selection-only graphs for the kernel breakdown
-    graphs, sel_graphs, att_graphs = [], [], []
+    # The timed loops replay CUDA graphs that run the L rotating layers back to back, as a
+    # model's decode step runs its layers: one graph per chain of all L layers (plus the
+    # partial chains a step count that is not a multiple of L needs), so no per-layer graph
+    # launch gap is timed. A "step" stays one layer's decode (cfg2: lps = 32 layers).
     launches_before = da.launch_count()
     with torch.cuda.stream(stream):
         for l in range(L):  # eager warm-up (also initialises the selection buffers)
             da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
     stream.synchronize()
     per_step_launches = (da.launch_count() - launches_before) // L * lps
-    for first in range(0, L, lps):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for l in range(first, first + lps):
-                da.decode_step(l, layers[l]["q"], layers[l]["out"], stream)
-        graphs.append(g)
-    for l in range(L):
-        _, stride, _ = da.last_selection(l)
-        ga = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(ga, stream=stream):
-            da.attend_selected(l, layers[l]["q"], layers[l]["out"], stream)
-        att_graphs.append(ga)
-        gs = torch.cuda.CUDAGraph()  # the step's own selection (fused kernel), no attention
-        with torch.cuda.graph(gs, stream=stream):
-            da.select_step(l, layers[l]["q"], stream)
-        sel_graphs.append((gs, None, None))
+    S = L // lps  # steps per chain
+
+    def chains(layer_fn):
+        """graphs[r] runs steps 0..r-1 of the chain (r = 1..S)."""
+        out = {}
+        for r in range(1, S + 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for l in range(r * lps):
+                    layer_fn(l)
+            out[r] = g
+        return out
+
+    step_chain = chains(lambda l: da.decode_step(l, layers[l]["q"], layers[l]["out"], stream))
+    att_chain = chains(lambda l: da.attend_selected(l, layers[l]["q"], layers[l]["out"], stream))
+    sel_chain = chains(lambda l: da.select_step(l, layers[l]["q"], stream))
 
     def sync_all():
         torch.cuda.synchronize()
@@ -429,10 +430,17 @@ def run_absp(args, w, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def run_steps(chain, steps):
+        """`steps` layer-steps as full chains plus one partial chain."""
+        for _ in range(steps // S):
+            chain[S].replay()
+        if steps % S:
+            chain[steps % S].replay()
+
     def timed(fn, steps, warm, sampler=None):
+        """fn(n): enqueue n steps on the stream; CUDA events around `steps` of them."""
         with torch.cuda.stream(stream):
-            for i in range(warm):
-                fn(i)
+            fn(warm)
         stream.synchronize()
         sync_all()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -441,8 +449,7 @@ def run_absp(args, w, rank, world, local):
             sampler.__enter__()
         with torch.cuda.stream(stream):
             e0.record(stream)
-            for i in range(steps):
-                fn(i)
+            fn(steps)
             e1.record(stream)
         e1.synchronize()
         if sampler:
@@ -451,7 +458,7 @@ def run_absp(args, w, rank, world, local):
         return max_over_ranks(e0.elapsed_time(e1) / steps)
 
     K, W = args.steps, max(args.warmup, 3)
-    step_fn = lambda i: graphs[i % len(graphs)].replay()
+    step_fn = lambda n: run_steps(step_chain, n)
     # clocks: a >= 100 ms window of the same step back to back just before the timed
     # region (the timed region itself can be ~1 ms), plus samples during the timed region
     window = ClockSampler(local, 0.002)
@@ -460,22 +467,22 @@ def run_absp(args, w, rank, world, local):
         t_end = time.perf_counter() + 0.12
         while time.perf_counter() < t_end:
             with torch.cuda.stream(stream):
-                for i in range(64):
-                    step_fn(i)
+                step_fn(64)
             reps += 64
             stream.synchronize()
     sampler = ClockSampler(local, 0.0)
     ms_step = timed(step_fn, K, W, sampler)
     trace(f"step timed: {ms_step * 1e3:.1f} us")
-    ms_attn = timed(lambda i: att_graphs[i % L].replay(), K, W)
-    ms_sel = timed(lambda i: sel_graphs[i % L][0].replay(), K, W)
+    # per-kernel breakdown: the attention alone and the selection alone, per layer
+    ms_attn = timed(lambda n: run_steps(att_chain, n), K, W) / lps
+    ms_sel = timed(lambda n: run_steps(sel_chain, n), K, W) / lps
 
     # optional all-gather of the per-rank outputs into the global [b][Hq][d] (reported
     # separately: the path itself exchanges nothing)
     gather_us = None
     if world > 1:
         sd = ShardedDecode(plan, lambda ql, ol: None, d, torch, device=dev, group=None)
-        ms_gather = timed(lambda i: sd.gather(), K, W)
+        ms_gather = timed(lambda n: [sd.gather() for _ in range(n)], K, W)
         gather_us = ms_gather * 1e3
 
     # end to end through the public C ABI with host buffers
@@ -574,8 +581,8 @@ def run_absp(args, w, rank, world, local):
             "roofline": {"bound": "hbm", "kernel": "k_attn (absp_attend_selected: paged flash-decode + fused LSE merge)",
                          "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "bytes_per_launch": attn_bytes,
-                         "peak_source": peak_src, "timing": "CUDA events over K back-to-back attention-only "
-                                                           "graph replays (rotating layers) / K"},
+                         "peak_source": peak_src, "timing": "CUDA events over K attention-only launches, the "
+                                                           "rotating layers back to back in one graph / K"},
             "step_roofline": {"bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms_step / 1e3) / 1e9,
                               "frac": step_bytes / (ms_step / 1e3) / 1e9 / peak},
             "kernels_us": {"step": ms_step * 1e3, "select": ms_sel * 1e3, "attend": ms_attn * 1e3,
