@@ -295,6 +295,7 @@ struct absp_ctx {
     int device = 0;
     int num_sms = 148;
     bool exact_select = false;  // ABSP_EXACT_SELECT=1: decode steps use the full exact scorer + top-k
+    uint32_t host_copy = 0;     // ABSP_HOST_STEP_COPY (diagnostics): bit 0 q, bit 1 out through copy nodes
     absp_config cfg{};
     std::vector<Layer> layers;
     uint64_t launches = 0;
@@ -703,6 +704,10 @@ absp_status absp_ctx_create(int device, const absp_config* cfg, absp_ctx** out) 
     ctx->num_sms = prop.multiProcessorCount;
     const char* es = std::getenv("ABSP_EXACT_SELECT");
     ctx->exact_select = es && es[0] == '1';
+    // diagnostics (tools/e2e_probe.py): host steps through copy nodes instead of the
+    // kernels addressing pinned host buffers (bit 0: q, bit 1: out)
+    const char* hc = std::getenv("ABSP_HOST_STEP_COPY");
+    ctx->host_copy = hc ? uint32_t(std::atoi(hc)) & 3u : 0u;
     ctx->cfg = *cfg;
     ctx->layers.resize(cfg->num_layers);
     *out = ctx;
@@ -1087,13 +1092,13 @@ static absp_status capture_host_step(absp_ctx* ctx, uint32_t layer, Layer* l, co
     // merges write it directly, unit by unit as they complete, instead of a copy after
     // the kernel. Otherwise (pageable, or not device-addressable) a D2H copy node.
     cudaPointerAttributes pa{};
-    const bool direct = cudaPointerGetAttributes(&pa, out_host) == cudaSuccess &&
+    const bool direct = !(ctx->host_copy & 2u) && cudaPointerGetAttributes(&pa, out_host) == cudaSuccess &&
                         pa.type == cudaMemoryTypeHost && pa.devicePointer == out_host;
     cudaGetLastError();
     // Likewise a device-addressable pinned q: the selection kernel reads it over PCIe
     // (one TMA copy of a unit's G rows per slice) and its finalizing CTAs leave each
     // unit's rows in stage_q for the attention, so there is no copy before the step.
-    const bool q_direct = fused_step_select(ctx, l) && cudaPointerGetAttributes(&pa, q_host) == cudaSuccess &&
+    const bool q_direct = !(ctx->host_copy & 1u) && fused_step_select(ctx, l) && cudaPointerGetAttributes(&pa, q_host) == cudaSuccess &&
                           pa.type == cudaMemoryTypeHost && pa.devicePointer == q_host;
     cudaGetLastError();
     cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);

@@ -60,3 +60,15 @@ b = wall(lambda: (gs.replay(), torch.cuda.synchronize()))
 c = wall(lambda: da.decode_step_host(0, qh, oh, stream))
 print(f"B={B}: empty graph {a:.1f} us | decode-step graph (device buffers) {b:.1f} us | "
       f"decode_step_host (pinned) {c:.1f} us")
+if "--copies" in sys.argv:  # the same with copy nodes instead of direct host access (diagnostics)
+    import os
+    res = {}
+    for mode, name in ((1, "q copy"), (2, "out copy"), (3, "both copies"), (0, "direct")):
+        os.environ["ABSP_HOST_STEP_COPY"] = str(mode)
+        dx = DecodeAttention(cfg)
+        dx.set_assignment(0, BlockAssignment.cycled(H, w["cands"]))
+        dx.bind(0, k, v, pt, [n] * B)
+        dx.build_store(0)
+        res[name] = wall(lambda: dx.decode_step_host(0, qh, oh, stream))
+        del dx
+    print("  " + " | ".join(f"{k} {v:.1f} us" for k, v in res.items()))
