@@ -12,12 +12,13 @@
 // one list; a persistent grid (one CTA per SM) takes contiguous ranges of it, so
 // every SM streams the same number of KV bytes whatever the block sizes.
 //
-// CTA = 8 consumer warps + 1 producer warp, 3-stage mbarrier ring of 64 KB stages:
-//   producer : lane s handles page slot s of the chunk two ahead (page list
-//              prefetched with independent loads) and issues one cp.async.bulk per
-//              page for K and V — the TMA bulk-copy engine, 1 instruction per 1-4 KB
-//              page — plus one for the unit's G query rows, completing on the
-//              stage's full barrier. In the decode step a unit is started as soon
+// CTA = 8 consumer warps + 2 or 4 producer warps, 3-stage mbarrier ring of 64 KB stages:
+//   producers: lane s handles page slot s of the chunk two ahead (page list
+//              prefetched with independent loads); even warps issue one cp.async.bulk
+//              per page for K, odd warps for V (4 warps for pages of <= 4 rows: each
+//              pair over half of the slots) — the TMA bulk-copy engine, 1 instruction
+//              per 1-4 KB page — and warp 0 one for the unit's G query rows, all
+//              completing on the stage's full barrier. In the decode step a unit is started as soon
 //              as its selection is published (per-unit ready flag, acquire), not
 //              when the whole top-k grid has finished. (A copy-only probe of this pipeline streams
 //              scattered 4 KB pages at 97% of measured HBM bandwidth.)
@@ -54,7 +55,11 @@ namespace {
 constexpr int kRows = kAttnChunkRows;    // 128 rows per chunk / stage
 constexpr int kWarps = kAttnSplits;      // consumer warps = splits per chunk (8)
 constexpr int kConsumers = 32 * kWarps;
-constexpr int kThreads = kConsumers + 32;  // + 1 producer warp
+// Producer warps per CTA (a template parameter chosen at launch from the page size,
+// attend_producers): even warps issue the K copies, odd ones the V copies. Two warps
+// while a stage is at most 32 bulk copies (pages of >= 8 rows); smaller pages take 4,
+// each pair over half of the page slots.
+__host__ __device__ constexpr int attend_producers(uint32_t P) { return 2 * (kRows / P) <= 32 ? 2 : 4; }
 constexpr int kStages = 3;
 constexpr int kWarpRows = kRows / kWarps;  // 16
 constexpr int kPStride = kWarpRows + 8;    // bf16 row stride of a P tile (bank-conflict free)
@@ -150,8 +155,8 @@ __device__ __forceinline__ uint32_t range_begin(uint32_t c, uint32_t W, uint32_t
     return uint32_t((uint64_t(c) * W) / C);
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
+template <int D, int NPROD>
+__global__ void __launch_bounds__(kConsumers + 32 * NPROD, 1) k_attn(LayerView L, const uint16_t* __restrict__ q,
                                                       PageList pages, uint32_t* __restrict__ ready,
                                                       const uint32_t* __restrict__ chunk_unit,
                                                       const uint32_t* __restrict__ chunk_idx,
@@ -173,12 +178,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     const uint32_t smem_base = smem_u32(smem);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    static_assert(NPROD == 2 || NPROD == 4, "producer warps come in K / V pairs");
+    constexpr uint32_t nprod = NPROD;
     const uint32_t w_begin = range_begin(blockIdx.x, n_work, gridDim.x);
     const uint32_t w_end = range_begin(blockIdx.x + 1, n_work, gridDim.x);
     // the producer's first 32 chunk descriptors (layout data, written before any step):
     // loaded before anything else so no fetch waits on them
     uint32_t cu_pre = 0, ci_pre = 0;
-    if (warp == kWarps && w_begin + lane < w_end) {
+    if (warp >= kWarps && w_begin + lane < w_end) {
         cu_pre = __ldg(chunk_unit + w_begin + lane);
         ci_pre = __ldg(chunk_idx + w_begin + lane);
     }
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     if (tid == 0) {
         sh.npend = 0u;
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(smem_u32(&sh.full[s]), 1);
+            mbar_init(smem_u32(&sh.full[s]), nprod);  // one arrive (+ expect_tx) per producer warp
             mbar_init(smem_u32(&sh.empty[s]), kWarps);  // every consumer warp
         }
         mbar_fence_init();
@@ -199,8 +206,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
     // raised after the top-k kernel's own wait); otherwise wait for the previous grid.
     if (!ready) griddep_wait();
 
-    if (warp == kWarps) {
-        // ============================ producer ================================
+    if (warp >= kWarps) {
+        // ============================ producers ===============================
+        // NPROD warps walk the same chunks: warp 0 writes the stage meta and issues the
+        // q copy, even warps the K copies, odd warps the V copies of their slot group.
+        // Bulk copies are issued one lane at a time, so one warp issuing a whole stage
+        // caps small pages (P = 4: 64 copies of 1 KB per stage) at ~3.3 TB/s; two warps
+        // reach ~5.9 TB/s (tools/bw_probe.cu, profiles/r2/bw_probe_producers.txt).
+        const uint32_t pw = warp - kWarps;
+        const bool kw = pw == 0, vw = (pw & 1) != 0;
+        constexpr uint32_t groups = nprod / 2;
+        const uint32_t grp = pw >> 1;  // slot group: slots s with s % groups == grp (groups: 1 or 2)
         // The page list (resolved by the top-k kernel, laid out by global chunk index)
         // of chunk w+2 is fetched while chunk w waits for a free stage: one round trip
         // of independent loads, two chunks ahead of the copy issue. Lane k*32+l owns
@@ -254,10 +270,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
             const uint32_t kdst = smem_base + stage * 2 * TB;
             const uint32_t full = smem_u32(&sh.full[stage]);
             uint32_t bytes = 0, invalid = 0;
+            if (!kw) {  // K or V copies of this warp's slot group only
+#pragma unroll
+                for (int k = 0; k < SPL; ++k) {
+                    const bool mine = vl[k] && ((k * 32 + lane) & (groups - 1)) == grp;
+                    bytes += __reduce_add_sync(0xffffffffu, mine ? P * D * 2 : 0u);
+                }
+                if (lane == 0) mbar_expect_tx(full, bytes);
+                __syncwarp();
+                const uint32_t dst0 = kdst + (vw ? TB : 0u);
+                const uint16_t* pool = vw ? L.v_pool : L.k_pool;
+#pragma unroll
+                for (int k = 0; k < SPL; ++k) {
+                    const uint32_t s = k * 32 + lane;
+                    if (s < NS && vl[k] && (s & (groups - 1)) == grp)
+                        bulk_g2s(dst0 + s * slot_stride, pool + size_t(gp[k]) * P * D, P * D * 2, full);
+                }
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
                 const uint32_t s = k * 32 + lane;
-                bytes += __reduce_add_sync(0xffffffffu, vl[k] ? 2 * P * D * 2 : 0u);
+                bytes += __reduce_add_sync(0xffffffffu, vl[k] && (s & (groups - 1)) == 0 ? P * D * 2 : 0u);
                 invalid |= __ballot_sync(0xffffffffu, s < NS && vl[k] < P);
                 // valid[] is stored by lane 0, the thread whose arrive on `full` (release)
                 // publishes the stage: 4 slots per word, gathered by shuffles
@@ -282,11 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_attn(LayerView L, const uint16_
 #pragma unroll
             for (int k = 0; k < SPL; ++k) {
                 const uint32_t s = k * 32 + lane;
-                if (s < NS && vl[k]) {
-                    const size_t off = size_t(gp[k]) * P * D;  // gp = head * pool_pages + page
-                    bulk_g2s(kdst + s * slot_stride, L.k_pool + off, P * D * 2, full);
-                    bulk_g2s(kdst + TB + s * slot_stride, L.v_pool + off, P * D * 2, full);
-                }
+                if (s < NS && vl[k] && (s & (groups - 1)) == 0)  // gp = head * pool_pages + page
+                    bulk_g2s(kdst + s * slot_stride, L.k_pool + size_t(gp[k]) * P * D, P * D * 2, full);
             }
             if (lane == 0) ATTN_TRACE(1 + (w - w_begin));  // producer issued chunk
             if (++stage == kStages) {
@@ -643,9 +678,12 @@ static uint32_t attend_hp(uint32_t D, uint32_t P, uint32_t G) {
 size_t attend_smem_bytes(uint32_t D, uint32_t P) { return attend_smem(D, P, attend_hp(D, P, 8)); }
 
 cudaError_t init_attend_attributes() {
-    cudaError_t e = cudaFuncSetAttribute(k_attn<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_attn<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (const void* f : {reinterpret_cast<const void*>(k_attn<64, 2>), reinterpret_cast<const void*>(k_attn<64, 4>),
+                          reinterpret_cast<const void*>(k_attn<128, 2>), reinterpret_cast<const void*>(k_attn<128, 4>)}) {
+        const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList& pages, uint32_t* ready,
@@ -656,12 +694,19 @@ cudaError_t launch_attend(const LayerView& L, const uint16_t* q, const PageList&
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const uint32_t grid = wk.grid;  // = min(n_work, SMs): the CTA runs in unit_run assume it
     if (grid == 0) return cudaSuccess;
-    if (L.D == 64)
-        launch_pdl(k_attn<64>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, ready, wk.chunk_unit, wk.chunk_idx,
-                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, hp, part_o, part_ml, wk.unit_done, out);
-    else
-        launch_pdl(k_attn<128>, dim3(grid), dim3(kThreads), smem, s, L, q, pages, ready, wk.chunk_unit, wk.chunk_idx,
-                   wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, hp, part_o, part_ml, wk.unit_done, out);
+    auto go = [&](auto kern, int nprod) {
+        launch_pdl(kern, dim3(grid), dim3(kConsumers + 32 * nprod), smem, s, L, q, pages, ready, wk.chunk_unit,
+                   wk.chunk_idx, wk.chunk_base, wk.unit_run, wk.n_work, wk.max_runs, hp, part_o, part_ml, wk.unit_done,
+                   out);
+    };
+    const int np = attend_producers(L.P);
+    if (L.D == 64) {
+        if (np == 2) go(k_attn<64, 2>, 2);
+        else go(k_attn<64, 4>, 4);
+    } else {
+        if (np == 2) go(k_attn<128, 2>, 2);
+        else go(k_attn<128, 4>, 4);
+    }
     ++*launches;
     return cudaGetLastError();
 }

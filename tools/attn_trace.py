@@ -13,7 +13,8 @@ import torch  # noqa: E402
 
 from paper_2605_12110_b200 import _abi  # noqa: E402
 
-_abi._lib = _abi.load(ROOT / "paper_2605_12110_b200" / "lib" / "libabsp_trace.so")
+import os  # noqa: E402
+_abi._lib = _abi.load(ROOT / "paper_2605_12110_b200" / "lib" / os.environ.get("ATTN_TRACE_LIB", "libabsp_trace.so"))
 _abi._lib.absp_debug_attn_trace.argtypes = [C.c_void_p, C.c_size_t]
 from bench import SEED, WORKLOADS  # noqa: E402
 from paper_2605_12110_b200 import (BlockAssignment, DecodeAttention, EngineConfig, QuantSpec,  # noqa: E402
@@ -47,6 +48,7 @@ _abi.check(_abi._lib.absp_debug_attn_trace(tr.ctypes.data, tr.nbytes))
 t0 = min(int(x) for x in tr[:148, 0] if x)
 rel = lambda x: (int(x) - t0) / 1000.0 if x else float("nan")
 firsts, gaps, leads, flushes, tails, ends, chunks = [], [], [], [], [], [], []
+fin_flush, fin_merge, npends = [], [], []
 for c in range(148):
     row = tr[c]
     arr = [rel(row[64 + i]) for i in range(64) if row[64 + i]]
@@ -63,6 +65,10 @@ for c in range(148):
     ends.append(max(rel(x) for x in row[242:250] if x))
     if row[240]:
         tails.append(ends[-1] - rel(row[240]))
+    npends.append(int(row[250]))
+    if row[240] and row[241]:
+        fin_flush.append(rel(row[241]) - rel(row[240]))
+        fin_merge.append(ends[-1] - rel(row[241]))
 pct = lambda a: f"median {statistics.median(a):6.2f}  p90 {np.percentile(a, 90):6.2f}  max {max(a):6.2f}" if a else "-"
 print(f"CTAs 148, chunks/CTA median {statistics.median(chunks)}")
 print(f"kernel span (first start -> last end)  {max(ends):.2f} us")
@@ -72,6 +78,8 @@ print(f"chunk inter-arrival at warp 0 (us)     {pct(gaps)}")
 print(f"issue -> data arrival (us)             {pct(leads)}")
 print(f"flush duration (us)                    {pct(flushes)}")
 print(f"final flush + merges (us)              {pct(tails)}")
+print(f"  final flush (us)                     {pct(fin_flush)}")
+print(f"  pending merges (us)                  {pct(fin_merge)}  (units merged at the end per CTA: {pct(npends)})")
 print(f"CTA end (us)                           {pct(ends)}")
 
 # ---- in-step timeline: flush L2, then a full decode step (top-k -> attention) ----

@@ -1,10 +1,12 @@
 #!/bin/bash
 # A/B of prebuilt library variants on the same box: bench lines (no CPU baseline) for each
 # workload, variants alternated twice. usage: tools/gpu_ab.sh <tag> <lib_a.so> <lib_b.so> ...
-# (libraries under paper_2605_12110_b200/lib/, selected per run through ABSP_LIB)
+# (libraries under paper_2605_12110_b200/lib/, selected per run through ABSP_LIB;
+# AB_WORKLOADS="cfg3,cfg5 --shard-of 8" overrides the workload list)
 TAG=$1; shift
 mkdir -p gpurun_out
-for A in "cfg3" "cfg3 --shard-of 8" "cfg3 --shard-of 2" "cfg5 --shard-of 8" "cfg1"; do
+IFS=',' read -ra WLS <<< "${AB_WORKLOADS:-cfg3,cfg3 --shard-of 8,cfg3 --shard-of 2,cfg5 --shard-of 8,cfg1}"
+for A in "${WLS[@]}"; do
   N=$(echo $A | tr ' ' '_' | tr -d '-')
   for rep in 1 2; do
     for LIBV in "$@"; do
