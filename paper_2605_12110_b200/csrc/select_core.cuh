@@ -32,7 +32,7 @@ constexpr uint32_t kRefineMin = 48;      // finalize: keys in the threshold bin 
 // Optional timeline instrumentation (debug builds with -DABSP_ATTN_TRACE): per CTA,
 // globaltimer stamps at the phase boundaries (tools/select_trace.py).
 #ifdef ABSP_ATTN_TRACE
-constexpr int kSelTraceSlots = 16;
+constexpr int kSelTraceSlots = 24;
 __device__ unsigned long long g_sel_trace[4096 * kSelTraceSlots];
 #define SEL_TRACE(slot)                                                                           \
     do {                                                                                          \
@@ -293,29 +293,36 @@ __device__ __forceinline__ void find_bin_desc(const uint32_t* hist, uint32_t kr,
     }
 }
 
-// Bitonic sort (descending) of n <= 1024 composites a[0, 1024), zero-padded, by the 8
-// consumer warps (4 elements per lane in registers: element warp*128 + 32 r + lane):
-// distances 32 and 64 inside a thread, below 32 by shuffles, 128 and up through shared
-// memory (6 of the 55 stages). The producer warp only joins the barriers.
-__device__ void sort1024_desc(unsigned long long* a, uint32_t n) {
+// Bitonic sort (descending) of n <= 256 R composites a[0, 256 R), zero-padded, by the 8
+// consumer warps (R elements per lane in registers: element warp*32R + 32 r + lane):
+// distances 32 .. 16R inside a thread (register indices resolved at compile time, so v
+// stays in registers), below 32 by shuffles, 32R and up through shared memory. The
+// producer warp only joins the barriers.
+template <int R>
+__device__ void sortreg_desc(unsigned long long* a, uint32_t n) {
+    constexpr uint32_t NE = 256u * R;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t i = n + tid; i < 1024u; i += blockDim.x) a[i] = 0ull;
+    for (uint32_t i = n + tid; i < NE; i += blockDim.x) a[i] = 0ull;
     __syncthreads();
+    SEL_TRACE(16);
     const bool act = warp < 8;
-    const uint32_t base = warp * 128 + lane;
-    unsigned long long v[4];
+    const uint32_t base = warp * 32u * R + lane;
+    unsigned long long v[R];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) v[r] = act ? a[base + 32 * r] : 0ull;
-    for (uint32_t k = 2; k <= 1024u; k <<= 1) {
-        uint32_t j = k >> 1;
-        if (j >= 128) {  // cross-warp distances through shared memory
+    for (int r = 0; r < R; ++r) v[r] = act ? a[base + 32 * r] : 0ull;
+    for (uint32_t k = 2; k <= NE; k <<= 1) {
+#ifdef SORT_PROBE
+        if (threadIdx.x == 0) g_sort_clk[31 - __clz(k)] = clock64();
+#endif
+        if ((k >> 1) >= 32u * R) {  // cross-warp distances through shared memory
+            if (k == 64u * R) SEL_TRACE(17);
             if (act) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) a[base + 32 * r] = v[r];
+                for (int r = 0; r < R; ++r) a[base + 32 * r] = v[r];
             }
             __syncthreads();
-            for (; j >= 128; j >>= 1) {
-                for (uint32_t i = tid; i < 1024u; i += blockDim.x) {
+            for (uint32_t j = k >> 1; j >= 32u * R; j >>= 1) {
+                for (uint32_t i = tid; i < NE; i += blockDim.x) {
                     const uint32_t ixj = i ^ j;
                     if (ixj > i) {
                         const unsigned long long x = a[i], y = a[ixj];
@@ -329,35 +336,38 @@ __device__ void sort1024_desc(unsigned long long* a, uint32_t n) {
             }
             if (act) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) v[r] = a[base + 32 * r];
+                for (int r = 0; r < R; ++r) v[r] = a[base + 32 * r];
             }
         }
         if (!act) continue;
-        for (; j >= 32; j >>= 1) {  // registers r and r | j/32 of this thread
-            const int rr = int(j >> 5);
+        const uint32_t j0 = min(k >> 1, 16u * R);
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                if (r & rr) continue;
+        for (int jr = R / 2; jr >= 1; jr >>= 1) {  // distance 32 jr: registers r and r | jr
+            if (uint32_t(32 * jr) > j0) continue;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (r & jr) continue;
                 const bool desc = ((base + 32 * r) & k) == 0;
-                const unsigned long long x = v[r], y = v[r | rr];
+                const unsigned long long x = v[r], y = v[r | jr];
                 const unsigned long long hi = x > y ? x : y, lo = x > y ? y : x;
                 v[r] = desc ? hi : lo;
-                v[r | rr] = desc ? lo : hi;
+                v[r | jr] = desc ? lo : hi;
             }
         }
-        for (; j > 0; j >>= 1) {  // lanes ^ j, same register
+        for (uint32_t j = min(k >> 1, 16u); j > 0; j >>= 1) {  // lanes ^ j, same register
             const bool lower = (lane & j) == 0;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < R; ++r) {
                 const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
                 const bool desc = ((base + 32 * r) & k) == 0;
                 v[r] = (lower == desc) ? (v[r] > o ? v[r] : o) : (v[r] > o ? o : v[r]);
             }
         }
     }
+    SEL_TRACE(18);
     if (act) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) a[base + 32 * r] = v[r];
+        for (int r = 0; r < R; ++r) a[base + 32 * r] = v[r];
     }
     __syncthreads();
 }
@@ -706,9 +716,13 @@ __device__ __forceinline__ void finalize_unit(const FinIn<D>& a, SelHead& sh) {
             above = trailing && me > ct;
             emit(rank + (trailing && ct > me ? 1u : 0u), ~uint32_t(me), j);
         }
-    } else if (n <= 1024u && reinterpret_cast<unsigned char*>(a.skeys) - reinterpret_cast<unsigned char*>(cand) >= 8192) {  // large sets (large budgets): sort (the 1024
-        // padded composites may overwrite the dead candidate list / pages), emit by position
-        sort1024_desc(cand, n);
+    } else if (n <= 2048u && reinterpret_cast<unsigned char*>(a.skeys) - reinterpret_cast<unsigned char*>(cand) >=
+                                 (n <= 1024u ? 8192 : 16384)) {
+        // large sets (large budgets): sort (the 1024 / 2048 padded composites may overwrite
+        // the dead candidate list / pages), emit by position
+        if (n <= 1024u) sortreg_desc<4>(cand, n);
+        else sortreg_desc<8>(cand, n);
+        SEL_TRACE(15);
         for (uint32_t p = tid; p < K1; p += kSThreads) {
             const unsigned long long me = cand[p];
             if (trailing && me > ct) atomicAdd(&sh.nsel, 1u);

@@ -177,6 +177,33 @@ def test_fused_select_ties(cuda, n, T):
         assert gl.step_selection[0][h].tolist() == list(range(k - 1)) + [n_blocks - 1]
 
 
+@pytest.mark.parametrize("tied", [600, 1500, 2500])
+def test_fused_select_large_candidate_sets(cuda, tied):
+    """A group of `tied` identical blocks outscores the rest (K = 512 of 10,000 blocks,
+    candidate capacity 2048): every group member is a candidate, so the finalize ranks
+    600 (register bitonic sort of 1024), 1500 (of 2048) or — past the capacity — runs
+    the exact fallback. The K - 1 lowest-indexed group blocks win, then the trailing block."""
+    from gpu_util import GpuLayer
+    n, P, b0, G = 40000, 4, 100, 2
+    rng = np.random.default_rng(tied)
+    pool_pages = n // P + 3
+    kf = (rng.standard_normal((2, pool_pages, P, 128)) * 0.05).astype(np.float32)
+    vf = rng.standard_normal((2, pool_pages, P, 128)).astype(np.float32)
+    layer = make_layer(9, H=2, G=G, d=128, P=P, block_sizes=(4,), seq_lens=(n,), kv=(kf, vf),
+                       q=np.ones((1, 2 * G, 128), np.float32))
+    kf = layer.k_pool  # bf16 bits [H][pages][P][d]
+    for t in range(4 * b0, 4 * (b0 + tied)):
+        kf[:, layer.page_table[0, t // P], t % P, :] = 0x3F80  # 1.0
+    gl = GpuLayer(layer, 2048)
+    sel = gl.select()
+    gl.decode()
+    _, _, want_sel, _ = oracle_step(layer, 0, 2048)
+    for h in range(2):
+        assert want_sel[h].tolist() == list(range(b0, b0 + 511)) + [n // 4 - 1], h
+        assert np.array_equal(sel[0][h], want_sel[h]), h
+        assert np.array_equal(gl.step_selection[0][h], want_sel[h]), ("decode step", h)
+
+
 def test_filter_error_bound(cuda):
     """select.cu's premise: |S_i - C_u - A_i| <= E per unit (with room to spare), so the
     candidate set provably contains the exact top-K."""

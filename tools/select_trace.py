@@ -56,7 +56,7 @@ for rep in range(2):
     torch.cuda.synchronize()
     g.replay()
     torch.cuda.synchronize()
-    st = np.zeros((4096, 16), np.uint64)
+    st = np.zeros((4096, 24), np.uint64)
     at = np.zeros((160, 256), np.uint64)
     _abi.check(_abi._lib.absp_debug_select_trace(st.ctypes.data, st.nbytes))
     _abi.check(_abi._lib.absp_debug_attn_trace(at.ctypes.data, at.nbytes))
@@ -81,3 +81,15 @@ for rep in range(2):
         print(f"  attn 1st data  {pct((fd[fd > 0].astype(np.float64) - t0) / 1e3)}")
         ends = at[live][:, 242:250].max(1)
         print(f"  attn end       {pct((ends.astype(np.float64) - t0) / 1e3)}")
+    if os.environ.get("SEL_TRACE_UNITS") == "1" and len(fin):
+        # per finalizing CTA: candidates and the durations of its finalize phases (us)
+        ph = [(7, "arrived"), (2, "loaded"), (11, "hist"), (13, "thr"), (8, "cands"), (9, "scored"),
+              (16, "s:zeroed"), (17, "s:smem"), (18, "s:end"), (15, "sorted"), (10, "ranked"), (12, "published")]
+        rows = []
+        for r in fin:
+            ts = [(nm, int(r[i])) for i, nm in ph if int(r[i]) >= t0]
+            d = {f"{a[0]}->{b[0]}": (b[1] - a[1]) / 1e3 for a, b in zip(ts, ts[1:])}
+            rows.append((int(r[14]), d))
+        rows.sort(key=lambda x: x[0])
+        for n_c, d in rows[:: max(1, len(rows) // 24)]:
+            print(f"    n={n_c:5d} " + " ".join(f"{k}={v:.2f}" for k, v in d.items()))
