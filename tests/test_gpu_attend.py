@@ -68,6 +68,9 @@ def _attend(gl, selection, stride):
     (64, 2, 16, (16, 32), (3000, 20), 5),                     # d = 64
     (128, 1, 4, (4, 16), (2500,), 200),                       # MHA, stride far above counts
     (128, 4, 16, (16, 48, 112), (5000, 700), 3),              # blocks that do not divide the 128-row chunk
+    (128, 4, 2, (2, 8, 32), (3001, 515), 7),                  # P = 2: 64 slots, 4 producer warps
+    (128, 2, 1, (1, 4, 16), (1500,), 2),                      # P = 1: 128 slots per chunk
+    (64, 4, 4, (4, 12, 32), (4099, 64), 11),                  # d = 64 with 4 producer warps
 ])
 def test_attend_random_selections_vs_oracle(cuda, d, G, P, cands, seq_lens, extra):
     from gpu_util import GpuLayer, within_tol

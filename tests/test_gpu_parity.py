@@ -85,6 +85,8 @@ def test_golden_cases(cuda, golden, name):
     (4, 8, 8, (8, 24, 40), (5000, 1234), 1024),               # block sizes that do not divide the 128-row
     (4, 8, 16, (16, 48, 80, 112), (9000, 777), 2048),         #   attention chunk (any multiple of P, as the
     (8, 4, 4, (12, 20), (3000,), 512),                        #   reference allows): chunks with empty slots
+    (4, 4, 2, (2, 8, 32), (3001, 515), 1024),                 # P = 2 and P = 1: 64 / 128 page slots per
+    (2, 4, 1, (1, 4), (1500,), 512),                          #   chunk, 4 attention producer warps
 ])
 def test_random_batches_vs_oracle(cuda, G, H, P, cands, seq_lens, T):
     from gpu_util import GpuLayer, within_tol
