@@ -25,6 +25,7 @@ def _bf16_values(rng, shape, scale=1.0):
     (4, 64, 16, (16, 32, 64), 256, 200, 90),     # crosses T (fallback -> sparse) and block boundaries
     (8, 128, 8, (8, 16, 32), 512, 1000, 40),     # cfg-1-like heads, P = 8
     (4, 128, 8, (8, 24, 40), 256, 230, 60),      # block sizes that do not divide the attention chunk
+    (4, 128, 4, (4, 8, 16), 256, 300, 50),       # P = 4: four attention producer warps
 ])
 def test_engine_steps_match_reference(cuda, H, d, P, cands, T, n0, steps):
     if not O.ref_available():
